@@ -1,0 +1,153 @@
+/* sph_b200.h — C-ABI drop-in for the reference SPH hot path on B200 (sm_100a).
+ *
+ * The reference's boundary is
+ *   KernelTimes soaview::sph::run_sweep(KernelId k, const CellGrid &grid,
+ *                                       const SphParams &par, Path path, Order order,
+ *                                       Guard guard, int threads = 1);
+ *   (/root/reference/proj/include/soaview/sph/kernels.hpp:45-46, kernels.cpp:861-872)
+ * which mutates the caller's 272-byte AoS `Particle` records (particle.hpp:11-46) in place
+ * through the per-cell `local` / `active` pointer lists of a `CellGrid` (grid.hpp:32-40).
+ *
+ * This header exposes the same operation as plain C: the caller flattens
+ * CellGrid::local into one `Particle*` array (cell-major) plus `cell_begin[ncells+1]`;
+ * the active lists are the reference's deduplicated, wrapped 3x3 stencil
+ * (grid.cpp:159-182) and are implied by (nx, ny). The library keeps a device-resident
+ * mirror of the records; sweeps run entirely on the GPU; sph_download writes back only
+ * the bytes the kernels wrote (each kernel's A_out, kernels.cpp:741-859, plus `flags`).
+ *
+ * Conventions: every function returns 0 on success and a negative SPH_E* code on error
+ * (details via sph_last_error). No C++ exceptions cross this boundary. Calls on one
+ * context are serialised by the caller; host pointers are borrowed for the call only.
+ * Integer selector values equal the reference enums (KernelId, Path, Order, Guard).
+ */
+#ifndef SPH_B200_H
+#define SPH_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SPH_B200_ABI_VERSION 1
+#define SPH_RECORD_SIZE 272 /* sizeof(soaview::sph::Particle), particle.hpp:40 */
+
+/* error codes */
+#define SPH_OK 0
+#define SPH_E_ARG -1     /* invalid argument */
+#define SPH_E_CUDA -2    /* CUDA runtime error (no device, OOM, launch failure) */
+#define SPH_E_STATE -3   /* call out of order (e.g. sweep before bind) */
+
+/* KernelId, kernels.hpp:9 */
+enum { SPH_DENSITY = 0, SPH_FORCE = 1, SPH_DRIFT = 2, SPH_KICK1 = 3, SPH_KICK2 = 4 };
+/* Path, kernels.hpp:13 */
+enum { SPH_PATH_AOS_BASELINE = 0, SPH_PATH_SOA_VIEW = 1 };
+/* Order, kernels.hpp:17 */
+enum { SPH_ORDER_LOCAL_ACTIVE = 0, SPH_ORDER_ACTIVE_LOCAL = 1 };
+/* Guard, kernels.hpp:20 */
+enum { SPH_GUARD_BRANCH = 0, SPH_GUARD_MASK = 1 };
+/* Device layout mode (the layout ablation). FROM_PATH maps AosBaseline -> AOS and
+ * SoaView -> CONVERT, mirroring the reference's two access paths. */
+enum { SPH_LAYOUT_FROM_PATH = -1, SPH_LAYOUT_AOS = 0, SPH_LAYOUT_CONVERT = 1,
+       SPH_LAYOUT_RESIDENT = 2 };
+/* Numerics. EXACT reproduces the reference's floating-point operation sequence (no FMA,
+ * IEEE sqrt/div, reference j order) and is byte-identical to the CPU. FAST uses FMA,
+ * rsqrt+Newton and hoisted per-j terms; results agree within the documented tolerance. */
+enum { SPH_NUMERICS_EXACT = 0, SPH_NUMERICS_FAST = 1 };
+
+typedef struct sph_ctx sph_ctx;
+
+/* SphParams, particle.hpp:49-55 (same field order). */
+typedef struct {
+  double dt, gamma, cfl, grav, target_wcount;
+} sph_params;
+
+/* KernelTimes, kernels.hpp:24-29 (device-measured: prologue = H2D/AoS->SoA,
+ * compute = kernels, epilogue = SoA->AoS/D2H). */
+typedef struct {
+  int64_t prologue_ns, compute_ns, epilogue_ns;
+} sph_times;
+
+typedef struct {
+  int64_t n;                  /* bound particles */
+  int32_t nx, ny, ncells;
+  int32_t layout, numerics;
+  int64_t active_pairs;       /* sum over cells of nl*na (one pass) */
+  int64_t density_pairs;      /* last density sweep: sum of nl*na*rounds */
+  int64_t density_updates;    /* last density sweep: particle-rounds */
+  int32_t density_rounds;     /* last density sweep: max rounds */
+  int32_t pad0;
+  int64_t density_failures;   /* last density sweep: particles that hit 30 rounds */
+  int64_t force_pairs;        /* last force sweep: sum of nl*na */
+  double last_density_ms, last_force_ms; /* device time of the pair kernels */
+} sph_stats;
+
+int sph_abi_version(void);
+
+/* Context lifetime (one per device; owns a CUDA stream). */
+int sph_create(int device, sph_ctx **out);
+void sph_destroy(sph_ctx *ctx);
+const char *sph_last_error(const sph_ctx *ctx);
+
+int sph_set_numerics(sph_ctx *ctx, int numerics);
+int sph_set_layout(sph_ctx *ctx, int layout);
+
+/* Bind a CellGrid. recs[k] for k in [cell_begin[c], cell_begin[c+1]) are the records of
+ * CellGrid::local[c] in list order; ncells = nx*ny. all_rank (optional, may be NULL) gives
+ * each record's index in ParticleStore::all, used to reproduce build_grid's list order on
+ * device rebins (grid.cpp:152-158); NULL means the flattened order itself. Uploads every
+ * record (all 272 bytes) to the device mirror. */
+int sph_bind(sph_ctx *ctx, void *const *recs, const int64_t *cell_begin, int nx, int ny,
+             double cell_size, const int64_t *all_rank);
+
+/* Re-upload all records (host mutated them); recs in the bound order. */
+int sph_upload(sph_ctx *ctx, void *const *recs);
+
+/* Write back the fields written on the device since the last upload/download (the A_out
+ * of each kernel run, plus flags); all other bytes of the host records stay untouched.
+ * recs are in the bound order (the device tracks rebins internally). */
+int sph_download(sph_ctx *ctx, void *const *recs);
+
+/* Write back every byte of every record. */
+int sph_download_all(sph_ctx *ctx, void *const *recs);
+
+/* One sweep of kernel `kernel` on the device mirror (no host traffic). */
+int sph_sweep(sph_ctx *ctx, int kernel, const sph_params *par, int path, int order, int guard,
+              sph_times *times);
+
+/* Drop-in for run_sweep on host records: upload (if the context is not already in sync),
+ * sweep, download of the kernel's A_out. times: prologue = H2D, epilogue = D2H. */
+int sph_run_sweep(sph_ctx *ctx, int kernel, void *const *recs, const sph_params *par,
+                  int path, int order, int guard, sph_times *times);
+
+/* Rebuild the cell lists on the device after particles moved (build_grid,
+ * grid.cpp:145-184): cell = clamp(floor(x*nx)), list order by ParticleStore::all rank. */
+int sph_rebin(sph_ctx *ctx);
+
+/* One leapfrog step on the device: kick1 -> drift -> rebin -> density -> force -> kick2.
+ * kernel_ms (optional, 6 entries) receives per-phase device time in that order. */
+int sph_step(sph_ctx *ctx, const sph_params *par, double *kernel_ms);
+
+/* make_particles (grid.cpp:76-143) on the device: the reference's deterministic IC
+ * (mt19937_64 on the host, then grid, mean_wcount, density, EOS and force with EXACT
+ * numerics, so records are byte-identical to the reference's) bound as a continuous
+ * store (ParticleStore::all sorted by (cell, id)). par_out receives the calibrated params. */
+int sph_make_particles(sph_ctx *ctx, int64_t n, int ppc, uint64_t seed, sph_params *par_out);
+
+/* Copy the mirror into a dense host array of n records in bound order (ParticleStore::all
+ * order for sph_make_particles contexts). */
+int sph_read_records(sph_ctx *ctx, void *out_records);
+
+int sph_get_stats(const sph_ctx *ctx, sph_stats *out);
+int sph_synchronize(sph_ctx *ctx);
+
+/* Measured FP64 FMA throughput of this device (TFLOP/s, 2 flops per DFMA). */
+int sph_fp64_peak(sph_ctx *ctx, double *tflops);
+
+/* Number of kernel launches issued by this library so far (for bench accounting). */
+int64_t sph_launch_count(const sph_ctx *ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SPH_B200_H */

@@ -1,0 +1,1017 @@
+// capi.cu — host runtime behind the C-ABI (include/sph_b200.h).
+//
+// Owns the device mirror of a bound CellGrid and drives the kernels. This replaces, in
+// order: the caller-side particle container traffic of run_sweep (the reference mutates
+// records through Particle* lists, kernels.cpp:861-872), the per-cell scheduler
+// (sweep_cells, kernels.cpp:492-533) with a GPU work list, the per-call SoA arenas
+// (layout.cpp) with resident device buffers, and build_grid (grid.cpp:145-184) with a
+// device rebin. make_particles (grid.cpp:76-143) runs its sweeps on the device with the
+// EXACT policy so the IC is byte-identical to the reference's.
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include <cub/cub.cuh>
+
+#include "../../include/sph_b200.h"
+#include "pair_kernels.cuh"
+#include "sph_kernels.h"
+
+using namespace sphb;
+
+namespace {
+
+struct CudaError {
+  cudaError_t e;
+  const char *what;
+  int line;
+};
+
+#define CK(call)                                                                           \
+  do {                                                                                     \
+    cudaError_t _e = (call);                                                               \
+    if (_e != cudaSuccess) throw CudaError{_e, #call, __LINE__};                          \
+  } while (0)
+
+struct ArgError {
+  std::string msg;
+};
+
+template <class T> struct DevBuf {
+  T *p = nullptr;
+  size_t cap = 0; // elements
+  void ensure(size_t n) {
+    if (n <= cap && p) return;
+    if (p) CK(cudaFree(p));
+    p = nullptr;
+    cap = 0;
+    CK(cudaMalloc(&p, std::max<size_t>(n, 1) * sizeof(T)));
+    cap = std::max<size_t>(n, 1);
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+  }
+};
+
+struct PinnedBuf {
+  void *p = nullptr;
+  size_t cap = 0;
+  void ensure(size_t bytes) {
+    if (bytes <= cap && p) return;
+    if (p) CK(cudaFreeHost(p));
+    p = nullptr;
+    cap = 0;
+    CK(cudaMallocHost(&p, std::max<size_t>(bytes, 64)));
+    cap = std::max<size_t>(bytes, 64);
+  }
+  void release() {
+    if (p) cudaFreeHost(p);
+    p = nullptr;
+    cap = 0;
+  }
+};
+
+// Host-side parallel loop (gathers/scatters between Particle* lists and pinned staging).
+template <class F> void parallel_for(int64_t n, F &&fn) {
+  int nt = (int)std::min<int64_t>(std::max(1u, std::thread::hardware_concurrency()), 32);
+  if (n < 65536 || nt <= 1) {
+    fn((int64_t)0, n);
+    return;
+  }
+  std::vector<std::thread> th;
+  int64_t chunk = (n + nt - 1) / nt;
+  for (int t = 0; t < nt; ++t) {
+    int64_t b = t * chunk, e = std::min(n, b + chunk);
+    if (b >= e) break;
+    th.emplace_back([&fn, b, e] { fn(b, e); });
+  }
+  for (auto &x : th) x.join();
+}
+
+struct HostField {
+  uint32_t bit;
+  int offset, size;
+};
+const HostField kHostFields[] = {
+    {F_X, 0, 16},       {F_V, 16, 16},      {F_VPRED, 32, 16},  {F_A, 48, 16},
+    {F_M, 64, 8},       {F_RHO, 72, 8},     {F_P, 80, 8},       {F_U, 88, 8},
+    {F_UPRED, 96, 8},   {F_UDT, 104, 8},    {F_C, 112, 8},      {F_H, 120, 8},
+    {F_WCOUNT, 128, 8}, {F_RHODH, 136, 8},  {F_ROTV, 144, 8},   {F_DIVV, 152, 8},
+    {F_VSIG, 160, 8},   {F_HDT, 168, 8},    {F_DTNEXT, 176, 8}, {F_FROZEN, 184, 4},
+    {F_MOVED, 188, 4},  {F_FLAGS, 208, 8},  {F_DBG, 216, 16},   {F_CELL, 200, 8},
+};
+
+uint32_t kernel_in(int k) {
+  switch (k) {
+  case SPH_DENSITY: return DEN_IN;
+  case SPH_FORCE: return FOR_IN;
+  case SPH_DRIFT: return DRIFT_IN;
+  case SPH_KICK1: return KICK1_IN;
+  default: return KICK2_IN;
+  }
+}
+uint32_t kernel_out(int k) {
+  switch (k) {
+  case SPH_DENSITY: return DEN_OUT;
+  case SPH_FORCE: return FOR_OUT;
+  case SPH_DRIFT: return DRIFT_OUT;
+  case SPH_KICK1: return KICK1_OUT;
+  default: return KICK2_OUT;
+  }
+}
+
+constexpr uint32_t kSoaFields = F_ALL_SOA & ~F_CELL; // fields with a SoA array
+
+// grid.cpp:23-26
+int grid_nx(int64_t n, int ppc) {
+  double cell = std::sqrt(static_cast<double>(ppc) / static_cast<double>(std::max<int64_t>(n, 1)));
+  return std::max(1, static_cast<int>(std::floor(1.0 / cell)));
+}
+
+// std::mt19937_64 (MT19937-64), grid.cpp:77 + unit_real grid.cpp:15-19.
+struct Mt64 {
+  uint64_t mt[312];
+  int mti;
+  explicit Mt64(uint64_t seed) {
+    mt[0] = seed;
+    for (int i = 1; i < 312; ++i) mt[i] = 6364136223846793005ULL * (mt[i - 1] ^ (mt[i - 1] >> 62)) + (uint64_t)i;
+    mti = 312;
+  }
+  uint64_t next() {
+    const uint64_t UM = 0xFFFFFFFF80000000ULL, LM = 0x7FFFFFFFULL, A = 0xB5026F5AA96619E9ULL;
+    if (mti >= 312) {
+      int i;
+      for (i = 0; i < 156; ++i) {
+        uint64_t x = (mt[i] & UM) | (mt[i + 1] & LM);
+        mt[i] = mt[i + 156] ^ (x >> 1) ^ ((x & 1ULL) ? A : 0ULL);
+      }
+      for (; i < 311; ++i) {
+        uint64_t x = (mt[i] & UM) | (mt[i + 1] & LM);
+        mt[i] = mt[i - 156] ^ (x >> 1) ^ ((x & 1ULL) ? A : 0ULL);
+      }
+      uint64_t x = (mt[311] & UM) | (mt[0] & LM);
+      mt[311] = mt[155] ^ (x >> 1) ^ ((x & 1ULL) ? A : 0ULL);
+      mti = 0;
+    }
+    uint64_t x = mt[mti++];
+    x ^= (x >> 29) & 0x5555555555555555ULL;
+    x ^= (x << 17) & 0x71D67FFFEDA60000ULL;
+    x ^= (x << 37) & 0xFFF7EEE000000000ULL;
+    x ^= (x >> 43);
+    return x;
+  }
+  double unit() { return static_cast<double>(next() >> 11) * 0x1.0p-53; }
+};
+
+} // namespace
+
+struct sph_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  std::string err;
+  int numerics = SPH_NUMERICS_FAST;
+  int layout = SPH_LAYOUT_FROM_PATH;
+
+  // geometry
+  bool bound = false;
+  int64_t n = 0;
+  int nx = 0, ny = 0, ncells = 0;
+  double cell_size = 0.0;
+  bool identity_order = true; // slot s holds bound record s (no rebin since bind)
+
+  // device state
+  DevBuf<Particle> aos, aos_tmp;
+  DevBuf<double2> f_x, f_v, f_vp, f_a, tmp2;
+  DevBuf<double> f_m, f_rho, f_p, f_u, f_upred, f_udt, f_c, f_h, f_wc, f_rdh, f_rot, f_div,
+      f_vsig, f_hdt, f_dtn, f_dbg0, tmp1;
+  DevBuf<int32_t> f_frozen, f_moved;
+  DevBuf<int64_t> f_flags, tmp8;
+  bool soa_alloc = false;
+  SoaMirror soa{};
+
+  DevBuf<int> cell_begin, cnt, pend_cnt, na_cell, ilist, pend_a, pend_b, host_idx, host_idx_tmp,
+      cellnew, vals, vals_sorted, scalars;
+  DevBuf<long long> all_rank, all_rank_tmp, pairs_dev;
+  DevBuf<unsigned long long> keys, keys_sorted;
+  DevBuf<Item> items0, items_a, items_b;
+  DevBuf<double> hcur, wc;
+  DevBuf<unsigned char> rounds;
+  DevBuf<char> dense, cub_tmp;
+  PinnedBuf h_stage, h_small;
+  int n_items0 = 0;
+  int64_t active_pairs = 0;
+
+  // mirror state
+  uint32_t dirty = 0;      // fields written on the device since the last host sync
+  bool soa_valid = false;  // SoA arrays hold current values of every SoA field
+  bool soa_ahead = false;  // SoA newer than AoS (resident mode)
+
+  sph_stats stats{};
+  int64_t launches = 0;
+  cudaEvent_t ev[16]{};
+
+  ~sph_ctx() {
+    for (auto &e : ev)
+      if (e) cudaEventDestroy(e);
+    if (stream) cudaStreamDestroy(stream);
+    aos.release(); aos_tmp.release();
+    f_x.release(); f_v.release(); f_vp.release(); f_a.release(); tmp2.release();
+    f_m.release(); f_rho.release(); f_p.release(); f_u.release(); f_upred.release();
+    f_udt.release(); f_c.release(); f_h.release(); f_wc.release(); f_rdh.release();
+    f_rot.release(); f_div.release(); f_vsig.release(); f_hdt.release(); f_dtn.release();
+    f_dbg0.release(); tmp1.release(); f_frozen.release(); f_moved.release(); f_flags.release();
+    tmp8.release(); cell_begin.release(); cnt.release(); pend_cnt.release(); na_cell.release();
+    ilist.release(); pend_a.release(); pend_b.release(); host_idx.release();
+    host_idx_tmp.release(); cellnew.release(); vals.release(); vals_sorted.release();
+    scalars.release(); all_rank.release(); all_rank_tmp.release(); pairs_dev.release();
+    keys.release(); keys_sorted.release(); items0.release(); items_a.release();
+    items_b.release(); hcur.release(); wc.release(); rounds.release(); dense.release();
+    cub_tmp.release(); h_stage.release(); h_small.release();
+  }
+
+  Geom geom() const {
+    Geom g;
+    g.nx = nx;
+    g.ny = ny;
+    g.ncells = ncells;
+    g.use_shift = (nx >= 5 && ny >= 5) ? 1 : 0;
+    g.cell_size = cell_size;
+    g.cell_begin = cell_begin.p;
+    return g;
+  }
+
+  void ensure_soa() {
+    const size_t N = (size_t)std::max<int64_t>(n, 1);
+    f_x.ensure(N); f_v.ensure(N); f_vp.ensure(N); f_a.ensure(N);
+    f_m.ensure(N); f_rho.ensure(N); f_p.ensure(N); f_u.ensure(N); f_upred.ensure(N);
+    f_udt.ensure(N); f_c.ensure(N); f_h.ensure(N); f_wc.ensure(N); f_rdh.ensure(N);
+    f_rot.ensure(N); f_div.ensure(N); f_vsig.ensure(N); f_hdt.ensure(N); f_dtn.ensure(N);
+    f_dbg0.ensure(N); f_frozen.ensure(N); f_moved.ensure(N); f_flags.ensure(N);
+    soa = SoaMirror{f_x.p, f_v.p, f_vp.p, f_a.p, f_m.p, f_rho.p, f_p.p, f_u.p, f_upred.p,
+                    f_udt.p, f_c.p, f_h.p, f_wc.p, f_rdh.p, f_rot.p, f_div.p, f_vsig.p,
+                    f_hdt.p, f_dtn.p, f_dbg0.p, f_frozen.p, f_moved.p, f_flags.p};
+    soa_alloc = true;
+  }
+
+  void alloc_for(int64_t nn, int nc) {
+    const size_t N = (size_t)std::max<int64_t>(nn, 1);
+    aos.ensure(N);
+    cell_begin.ensure(nc + 1);
+    cnt.ensure(nc);
+    pend_cnt.ensure(nc);
+    na_cell.ensure(nc);
+    ilist.ensure(N);
+    pend_a.ensure(N);
+    pend_b.ensure(N);
+    host_idx.ensure(N);
+    all_rank.ensure(N);
+    hcur.ensure(N);
+    rounds.ensure(N);
+    scalars.ensure(4);
+    pairs_dev.ensure(2);
+    // worst case items: one per cell + n / kTI
+    const size_t it = (size_t)nc + N / kTI + 1;
+    items0.ensure(it);
+    items_a.ensure(it);
+    items_b.ensure(it);
+    h_small.ensure(64);
+  }
+
+  void launched(int k = 1) { launches += k; }
+
+  // Work list + derived per-cell data after the slot order changed.
+  void rebuild_worklist() {
+    launch_cell_counts(na_cell.p, cnt.p, cell_begin.p, nx, ny, stream);
+    const bool aos_src = !soa_ahead;
+    launch_spatial_order(ilist.p, aos.p, soa, aos_src, cell_begin.p, ncells, nx, ny, stream);
+    launch_make_items(items0.p, scalars.p, pairs_dev.p, cnt.p, cell_begin.p, na_cell.p, ncells,
+                      stream);
+    launched(3);
+    CK(cudaMemcpyAsync(h_small.p, scalars.p, sizeof(int), cudaMemcpyDeviceToHost, stream));
+    CK(cudaMemcpyAsync((char *)h_small.p + 8, pairs_dev.p, sizeof(long long),
+                       cudaMemcpyDeviceToHost, stream));
+    CK(cudaStreamSynchronize(stream));
+    n_items0 = *(int *)h_small.p;
+    active_pairs = *(long long *)((char *)h_small.p + 8);
+    stats.active_pairs = active_pairs;
+  }
+
+  // ---- mirror coherence ----
+  void make_aos_current() {
+    if (soa_ahead) {
+      launch_scatter(aos.p, soa, (int)n, kSoaFields, stream);
+      launched();
+      soa_ahead = false;
+    }
+  }
+  void make_soa_current() {
+    ensure_soa();
+    if (!soa_valid) {
+      launch_gather(aos.p, soa, (int)n, kSoaFields, stream);
+      launched();
+      soa_valid = true;
+    }
+  }
+
+  // ---- sweeps ----
+  int mode_for(int path) const {
+    if (layout == SPH_LAYOUT_FROM_PATH) return path == SPH_PATH_SOA_VIEW ? SPH_LAYOUT_CONVERT : SPH_LAYOUT_AOS;
+    return layout;
+  }
+
+  void run_density(bool use_aos, bool exact, const Params &par, bool meanw) {
+    DenArgs A{};
+    A.g = geom();
+    A.target = par.target_wcount;
+    A.h_max = cell_size / kSupport; // kernels.cpp:542
+    A.aos = aos.p;
+    A.soa = soa;
+    A.hcur = hcur.p;
+    A.pend_cnt = pend_cnt.p;
+    A.rounds_out = rounds.p;
+    A.wc_out = wc.p;
+    const Item *items = items0.p;
+    const int *list = ilist.p;
+    int nitems = n_items0;
+    int64_t pairs = active_pairs, pairs_total = 0, updates = 0;
+    int max_round = 0;
+    int *pend_out = pend_a.p;
+    Item *items_next = items_a.p;
+    for (int r = 0; r < 30 && nitems > 0; ++r) {
+      A.items = items;
+      A.list = list;
+      A.round = r;
+      A.pend_list = pend_out;
+      if (meanw) {
+        launch_density_exact(A, nitems, use_aos, true, stream);
+        launched();
+        break;
+      }
+      CK(cudaMemsetAsync(pend_cnt.p, 0, sizeof(int) * ncells, stream));
+      if (exact) launch_density_exact(A, nitems, use_aos, false, stream);
+      else launch_density_fast(A, nitems, use_aos, stream);
+      launch_make_items(items_next, scalars.p, pairs_dev.p, pend_cnt.p, cell_begin.p, na_cell.p,
+                        ncells, stream);
+      launched(2);
+      pairs_total += pairs;
+      max_round = r + 1;
+      CK(cudaMemcpyAsync(h_small.p, scalars.p, sizeof(int), cudaMemcpyDeviceToHost, stream));
+      CK(cudaMemcpyAsync((char *)h_small.p + 8, pairs_dev.p, sizeof(long long),
+                         cudaMemcpyDeviceToHost, stream));
+      CK(cudaStreamSynchronize(stream));
+      nitems = *(int *)h_small.p;
+      pairs = *(long long *)((char *)h_small.p + 8);
+      // next round reads what this one wrote
+      items = items_next;
+      list = pend_out;
+      items_next = (items_next == items_a.p) ? items_b.p : items_a.p;
+      pend_out = (pend_out == pend_a.p) ? pend_b.p : pend_a.p;
+    }
+    if (!meanw) {
+      stats.density_pairs = pairs_total;
+      stats.density_rounds = max_round;
+      (void)updates;
+    }
+  }
+
+  void run_force(bool use_aos, bool exact, const Params &par) {
+    ForArgs A{};
+    A.g = geom();
+    A.items = items0.p;
+    A.list = ilist.p;
+    A.grav = par.grav;
+    A.aos = aos.p;
+    A.soa = soa;
+    if (exact) launch_force_exact(A, n_items0, use_aos, stream);
+    else launch_force_fast(A, n_items0, use_aos, stream);
+    launched();
+    stats.force_pairs = active_pairs;
+  }
+
+  // One sweep on the device. Events: ev[0..3] bracket prologue / compute / epilogue.
+  void sweep(int kernel, const Params &par, int path) {
+    const int mode = mode_for(path);
+    const bool exact = numerics == SPH_NUMERICS_EXACT;
+    if (mode == SPH_LAYOUT_RESIDENT) {
+      make_soa_current();
+    } else {
+      make_aos_current();
+      if (mode == SPH_LAYOUT_CONVERT) ensure_soa();
+    }
+    CK(cudaEventRecord(ev[0], stream));
+    if (mode == SPH_LAYOUT_CONVERT) {
+      launch_gather(aos.p, soa, (int)n, kernel_in(kernel), stream); // AoS -> SoA view
+      launched();
+    }
+    CK(cudaEventRecord(ev[1], stream));
+    const bool use_aos = mode == SPH_LAYOUT_AOS;
+    if (kernel == SPH_DENSITY) run_density(use_aos, exact, par, false);
+    else if (kernel == SPH_FORCE) run_force(use_aos, exact, par);
+    else {
+      launch_linear(kernel, use_aos, aos.p, soa, (int)n, par, stream);
+      launched();
+    }
+    CK(cudaEventRecord(ev[2], stream));
+    if (mode == SPH_LAYOUT_CONVERT) {
+      launch_scatter(aos.p, soa, (int)n, kernel_out(kernel), stream); // SoA -> AoS (Out/InOut)
+      launched();
+    }
+    CK(cudaEventRecord(ev[3], stream));
+    if (mode == SPH_LAYOUT_RESIDENT) soa_ahead = true;
+    else soa_valid = false;
+    dirty |= kernel_out(kernel);
+  }
+
+  // ---- host <-> device ----
+  bool contiguous(void *const *recs) const {
+    const char *b = static_cast<const char *>(recs[0]);
+    for (int64_t k = 1; k < n; ++k)
+      if (static_cast<const char *>(recs[k]) != b + k * SPH_RECORD_SIZE) return false;
+    return true;
+  }
+
+  // Full records, bound order -> device slots.
+  void upload_full(void *const *recs) {
+    const size_t bytes = (size_t)n * SPH_RECORD_SIZE;
+    if (n == 0) return;
+    const void *src;
+    if (contiguous(recs)) {
+      src = recs[0];
+    } else {
+      h_stage.ensure(bytes);
+      char *st = static_cast<char *>(h_stage.p);
+      parallel_for(n, [&](int64_t b, int64_t e) {
+        for (int64_t k = b; k < e; ++k) std::memcpy(st + k * SPH_RECORD_SIZE, recs[k], SPH_RECORD_SIZE);
+      });
+      src = h_stage.p;
+    }
+    if (identity_order) {
+      CK(cudaMemcpyAsync(aos.p, src, bytes, cudaMemcpyHostToDevice, stream));
+    } else {
+      dense.ensure(bytes);
+      CK(cudaMemcpyAsync(dense.p, src, bytes, cudaMemcpyHostToDevice, stream));
+      launch_expand(aos.p, reinterpret_cast<Particle *>(dense.p), host_idx.p, (int)n, stream);
+      launched();
+    }
+    soa_valid = false;
+    soa_ahead = false;
+    dirty = 0;
+  }
+
+  // Fields in `mask`, bound order -> device slots (AoS). Returns H2D bytes.
+  size_t upload_fields(void *const *recs, uint32_t mask);
+
+  // Device -> host: the fields in `mask` (default: dirty). Returns D2H bytes.
+  size_t download_fields(void *const *recs, uint32_t mask) {
+    if (n == 0 || !mask) return 0;
+    make_aos_current();
+    const size_t per = packed_bytes_per_record(mask);
+    const size_t bytes = per * (size_t)n;
+    dense.ensure(bytes);
+    h_stage.ensure(bytes);
+    launch_pack(dense.p, aos.p, host_idx.p, (int)n, mask, stream);
+    launched();
+    CK(cudaMemcpyAsync(h_stage.p, dense.p, bytes, cudaMemcpyDeviceToHost, stream));
+    CK(cudaStreamSynchronize(stream));
+    const char *st = static_cast<const char *>(h_stage.p);
+    // per-field blocks, ascending field order (pack_kernel layout)
+    std::vector<std::pair<HostField, size_t>> fl;
+    size_t base = 0;
+    for (const HostField &f : kHostFields)
+      if (mask & f.bit) {
+        fl.push_back({f, base});
+        base += (size_t)f.size * (size_t)n;
+      }
+    parallel_for(n, [&](int64_t b, int64_t e) {
+      for (int64_t k = b; k < e; ++k) {
+        char *rec = static_cast<char *>(recs[k]);
+        for (auto &pf : fl)
+          std::memcpy(rec + pf.first.offset, st + pf.second + (size_t)k * pf.first.size, pf.first.size);
+      }
+    });
+    return bytes;
+  }
+
+  void download_all(void *const *recs) {
+    if (n == 0) return;
+    make_aos_current();
+    const size_t bytes = (size_t)n * SPH_RECORD_SIZE;
+    const bool contig = contiguous(recs);
+    void *dst = contig ? recs[0] : (h_stage.ensure(bytes), h_stage.p);
+    if (identity_order) {
+      CK(cudaMemcpyAsync(dst, aos.p, bytes, cudaMemcpyDeviceToHost, stream));
+    } else {
+      dense.ensure(bytes);
+      launch_compact(reinterpret_cast<Particle *>(dense.p), aos.p, host_idx.p, (int)n, stream);
+      launched();
+      CK(cudaMemcpyAsync(dst, dense.p, bytes, cudaMemcpyDeviceToHost, stream));
+    }
+    CK(cudaStreamSynchronize(stream));
+    if (!contig) {
+      const char *st = static_cast<const char *>(h_stage.p);
+      parallel_for(n, [&](int64_t b, int64_t e) {
+        for (int64_t k = b; k < e; ++k) std::memcpy(recs[k], st + k * SPH_RECORD_SIZE, SPH_RECORD_SIZE);
+      });
+    }
+    dirty = 0;
+  }
+
+  void bind(void *const *recs, const int64_t *cb64, int nx_, int ny_, double cs,
+            const int64_t *rank) {
+    if (nx_ <= 0 || ny_ <= 0) throw ArgError{"nx and ny must be positive"};
+    const int nc = nx_ * ny_;
+    const int64_t nn = cb64[nc];
+    if (nn < 0 || nn >= (1LL << 31)) throw ArgError{"particle count out of range"};
+    if (cb64[0] != 0) throw ArgError{"cell_begin[0] must be 0"};
+    std::vector<int> cb(nc + 1);
+    for (int c = 0; c <= nc; ++c) {
+      if (c > 0 && cb64[c] < cb64[c - 1]) throw ArgError{"cell_begin must be non-decreasing"};
+      cb[c] = (int)cb64[c];
+    }
+    for (int64_t k = 0; k < nn; ++k)
+      if (!recs[k]) throw ArgError{"null record pointer"};
+    n = nn;
+    nx = nx_;
+    ny = ny_;
+    ncells = nc;
+    cell_size = cs;
+    alloc_for(n, nc);
+    soa_valid = false;
+    soa_ahead = false;
+    identity_order = true;
+    CK(cudaMemcpyAsync(cell_begin.p, cb.data(), sizeof(int) * (nc + 1), cudaMemcpyHostToDevice, stream));
+    std::vector<int> hid(std::max<int64_t>(n, 1));
+    std::vector<long long> ar(std::max<int64_t>(n, 1));
+    for (int64_t k = 0; k < n; ++k) {
+      hid[k] = (int)k;
+      ar[k] = rank ? (long long)rank[k] : (long long)k;
+    }
+    CK(cudaMemcpyAsync(host_idx.p, hid.data(), sizeof(int) * n, cudaMemcpyHostToDevice, stream));
+    CK(cudaMemcpyAsync(all_rank.p, ar.data(), sizeof(long long) * n, cudaMemcpyHostToDevice, stream));
+    upload_full(recs);
+    rebuild_worklist(); // synchronises (host vectors above stay alive until then)
+    bound = true;
+    stats = sph_stats{};
+    stats.n = n;
+    stats.nx = nx;
+    stats.ny = ny;
+    stats.ncells = ncells;
+    stats.active_pairs = active_pairs;
+  }
+
+  void rebin() {
+    if (n == 0) return;
+    const bool soa_src = soa_ahead;
+    keys.ensure(n); keys_sorted.ensure(n); vals.ensure(n); vals_sorted.ensure(n); cellnew.ensure(n);
+    launch_rebin_keys(keys.p, vals.p, cellnew.p, aos.p, soa, !soa_src, all_rank.p, (int)n, nx, ny, stream);
+    launched();
+    int end_bit = 40;
+    while ((1LL << (end_bit - 40)) < ncells) ++end_bit;
+    size_t tmp_bytes = 0;
+    CK(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, keys.p, keys_sorted.p, vals.p,
+                                       vals_sorted.p, (int)n, 0, end_bit, stream));
+    cub_tmp.ensure(tmp_bytes);
+    CK(cub::DeviceRadixSort::SortPairs(cub_tmp.p, tmp_bytes, keys.p, keys_sorted.p, vals.p,
+                                       vals_sorted.p, (int)n, 0, end_bit, stream));
+    launched(4);
+    const int *perm = vals_sorted.p;
+    launch_cell_begin_from_sorted(cell_begin.p, keys_sorted.p, (int)n, ncells, stream);
+    aos_tmp.ensure(n);
+    launch_permute<Particle>(aos_tmp.p, aos.p, perm, (int)n, stream);
+    std::swap(aos.p, aos_tmp.p);
+    std::swap(aos.cap, aos_tmp.cap);
+    host_idx_tmp.ensure(n);
+    launch_permute<int>(host_idx_tmp.p, host_idx.p, perm, (int)n, stream);
+    std::swap(host_idx.p, host_idx_tmp.p);
+    std::swap(host_idx.cap, host_idx_tmp.cap);
+    all_rank_tmp.ensure(n);
+    launch_permute<long long>(all_rank_tmp.p, all_rank.p, perm, (int)n, stream);
+    std::swap(all_rank.p, all_rank_tmp.p);
+    std::swap(all_rank.cap, all_rank_tmp.cap);
+    launched(4);
+    if (soa_valid || soa_ahead) {
+      auto p2 = [&](DevBuf<double2> &b) {
+        tmp2.ensure(n);
+        launch_permute<double2>(tmp2.p, b.p, perm, (int)n, stream);
+        std::swap(b.p, tmp2.p);
+        std::swap(b.cap, tmp2.cap);
+        launched();
+      };
+      auto p1 = [&](DevBuf<double> &b) {
+        tmp1.ensure(n);
+        launch_permute<double>(tmp1.p, b.p, perm, (int)n, stream);
+        std::swap(b.p, tmp1.p);
+        std::swap(b.cap, tmp1.cap);
+        launched();
+      };
+      p2(f_x); p2(f_v); p2(f_vp); p2(f_a);
+      p1(f_m); p1(f_rho); p1(f_p); p1(f_u); p1(f_upred); p1(f_udt); p1(f_c); p1(f_h);
+      p1(f_wc); p1(f_rdh); p1(f_rot); p1(f_div); p1(f_vsig); p1(f_hdt); p1(f_dtn); p1(f_dbg0);
+      {
+        // frozen / moved (int32) and flags (int64) through the scratch int / int64 buffers
+        vals.ensure(n);
+        launch_permute<int>(vals.p, f_frozen.p, perm, (int)n, stream);
+        std::swap(f_frozen.p, vals.p);
+        std::swap(f_frozen.cap, vals.cap);
+        launch_permute<int>(vals.p, f_moved.p, perm, (int)n, stream);
+        std::swap(f_moved.p, vals.p);
+        std::swap(f_moved.cap, vals.cap);
+        tmp8.ensure(n);
+        launch_permute<int64_t>(tmp8.p, f_flags.p, perm, (int)n, stream);
+        std::swap(f_flags.p, tmp8.p);
+        std::swap(f_flags.cap, tmp8.cap);
+        launched(3);
+      }
+      soa = SoaMirror{f_x.p, f_v.p, f_vp.p, f_a.p, f_m.p, f_rho.p, f_p.p, f_u.p, f_upred.p,
+                      f_udt.p, f_c.p, f_h.p, f_wc.p, f_rdh.p, f_rot.p, f_div.p, f_vsig.p,
+                      f_hdt.p, f_dtn.p, f_dbg0.p, f_frozen.p, f_moved.p, f_flags.p};
+    }
+    launch_set_cell(aos.p, cell_begin.p, ncells, stream); // build_grid writes p->cell (grid.cpp:156)
+    launched();
+    dirty |= F_CELL;
+    identity_order = false;
+    rebuild_worklist();
+  }
+};
+
+size_t sph_ctx::upload_fields(void *const *recs, uint32_t mask) {
+  if (n == 0 || !mask) return 0;
+  make_aos_current();
+  // host pack: per-field blocks in bound order, then device unpack into slots
+  std::vector<std::pair<HostField, size_t>> fl;
+  size_t base = 0;
+  for (const HostField &f : kHostFields)
+    if (mask & f.bit) {
+      fl.push_back({f, base});
+      base += (size_t)f.size * (size_t)n;
+    }
+  h_stage.ensure(base);
+  char *st = static_cast<char *>(h_stage.p);
+  parallel_for(n, [&](int64_t b, int64_t e) {
+    for (int64_t k = b; k < e; ++k) {
+      const char *rec = static_cast<const char *>(recs[k]);
+      for (auto &pf : fl)
+        std::memcpy(st + pf.second + (size_t)k * pf.first.size, rec + pf.first.offset, pf.first.size);
+    }
+  });
+  dense.ensure(base);
+  CK(cudaMemcpyAsync(dense.p, st, base, cudaMemcpyHostToDevice, stream));
+  launch_unpack_fields(aos.p, dense.p, host_idx.p, (int)n, mask, stream);
+  launched();
+  soa_valid = false;
+  return base;
+}
+
+// ---------------------------------------------------------------------------------------
+// C ABI
+// ---------------------------------------------------------------------------------------
+namespace {
+template <class F> int guarded(sph_ctx *ctx, F &&fn) {
+  if (!ctx) return SPH_E_ARG;
+  try {
+    CK(cudaSetDevice(ctx->device));
+    int r = fn();
+    if (r == SPH_OK) ctx->err.clear();
+    return r;
+  } catch (const CudaError &e) {
+    char buf[512];
+    std::snprintf(buf, sizeof buf, "CUDA error %s (%s) in %s [capi.cu:%d]", cudaGetErrorName(e.e),
+                  cudaGetErrorString(e.e), e.what, e.line);
+    ctx->err = buf;
+    cudaGetLastError();
+    return SPH_E_CUDA;
+  } catch (const ArgError &e) {
+    ctx->err = e.msg;
+    return SPH_E_ARG;
+  } catch (const std::bad_alloc &) {
+    ctx->err = "host out of memory";
+    return SPH_E_CUDA;
+  }
+}
+
+Params to_params(const sph_params *p) {
+  return Params{p->dt, p->gamma, p->cfl, p->grav, p->target_wcount};
+}
+
+void check_kernel(int k) {
+  if (k < SPH_DENSITY || k > SPH_KICK2) throw ArgError{"unknown kernel id"};
+}
+} // namespace
+
+extern "C" {
+
+int sph_abi_version(void) { return SPH_B200_ABI_VERSION; }
+
+int sph_create(int device, sph_ctx **out) {
+  if (!out) return SPH_E_ARG;
+  *out = nullptr;
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev <= 0) {
+    cudaGetLastError();
+    return SPH_E_CUDA;
+  }
+  if (device < 0 || device >= ndev) return SPH_E_ARG;
+  sph_ctx *ctx = new (std::nothrow) sph_ctx;
+  if (!ctx) return SPH_E_CUDA;
+  ctx->device = device;
+  int r = guarded(ctx, [&] {
+    CK(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
+    for (auto &e : ctx->ev) CK(cudaEventCreate(&e));
+    return SPH_OK;
+  });
+  if (r != SPH_OK) {
+    delete ctx;
+    return r;
+  }
+  *out = ctx;
+  return SPH_OK;
+}
+
+void sph_destroy(sph_ctx *ctx) {
+  if (!ctx) return;
+  cudaSetDevice(ctx->device);
+  delete ctx;
+}
+
+const char *sph_last_error(const sph_ctx *ctx) { return ctx ? ctx->err.c_str() : "null context"; }
+
+int sph_set_numerics(sph_ctx *ctx, int numerics) {
+  return guarded(ctx, [&] {
+    if (numerics != SPH_NUMERICS_EXACT && numerics != SPH_NUMERICS_FAST) throw ArgError{"bad numerics"};
+    ctx->numerics = numerics;
+    ctx->stats.numerics = numerics;
+    return SPH_OK;
+  });
+}
+
+int sph_set_layout(sph_ctx *ctx, int layout) {
+  return guarded(ctx, [&] {
+    if (layout < SPH_LAYOUT_FROM_PATH || layout > SPH_LAYOUT_RESIDENT) throw ArgError{"bad layout"};
+    ctx->layout = layout;
+    ctx->stats.layout = layout;
+    return SPH_OK;
+  });
+}
+
+int sph_bind(sph_ctx *ctx, void *const *recs, const int64_t *cell_begin, int nx, int ny,
+             double cell_size, const int64_t *all_rank) {
+  return guarded(ctx, [&] {
+    if (!cell_begin || (!recs && cell_begin[(size_t)nx * ny] > 0)) throw ArgError{"null argument"};
+    ctx->bind(recs, cell_begin, nx, ny, cell_size, all_rank);
+    return SPH_OK;
+  });
+}
+
+int sph_upload(sph_ctx *ctx, void *const *recs) {
+  return guarded(ctx, [&] {
+    if (!ctx->bound) throw ArgError{"sph_upload before sph_bind"};
+    ctx->upload_full(recs);
+    CK(cudaStreamSynchronize(ctx->stream));
+    return SPH_OK;
+  });
+}
+
+int sph_download(sph_ctx *ctx, void *const *recs) {
+  return guarded(ctx, [&] {
+    if (!ctx->bound) throw ArgError{"sph_download before sph_bind"};
+    ctx->download_fields(recs, ctx->dirty);
+    ctx->dirty = 0;
+    return SPH_OK;
+  });
+}
+
+int sph_download_all(sph_ctx *ctx, void *const *recs) {
+  return guarded(ctx, [&] {
+    if (!ctx->bound) throw ArgError{"sph_download_all before sph_bind"};
+    ctx->download_all(recs);
+    return SPH_OK;
+  });
+}
+
+int sph_read_records(sph_ctx *ctx, void *out) {
+  return guarded(ctx, [&] {
+    if (!ctx->bound) throw ArgError{"sph_read_records before sph_bind"};
+    std::vector<void *> ptrs(std::max<int64_t>(ctx->n, 1));
+    for (int64_t k = 0; k < ctx->n; ++k) ptrs[k] = static_cast<char *>(out) + k * SPH_RECORD_SIZE;
+    ctx->download_all(ptrs.data());
+    return SPH_OK;
+  });
+}
+
+int sph_sweep(sph_ctx *ctx, int kernel, const sph_params *par, int path, int order, int guard,
+              sph_times *times) {
+  (void)order; // LocalActive / ActiveLocal are bitwise-equivalent (test_sph.cpp:319-328)
+  (void)guard; // Branch / Mask are bitwise-equivalent (test_sph.cpp:308-317)
+  return guarded(ctx, [&] {
+    if (!ctx->bound) throw ArgError{"sph_sweep before sph_bind"};
+    if (!par) throw ArgError{"null params"};
+    check_kernel(kernel);
+    ctx->sweep(kernel, to_params(par), path);
+    CK(cudaStreamSynchronize(ctx->stream));
+    float a = 0, b = 0, c = 0;
+    CK(cudaEventElapsedTime(&a, ctx->ev[0], ctx->ev[1]));
+    CK(cudaEventElapsedTime(&b, ctx->ev[1], ctx->ev[2]));
+    CK(cudaEventElapsedTime(&c, ctx->ev[2], ctx->ev[3]));
+    if (kernel == SPH_DENSITY) ctx->stats.last_density_ms = b;
+    if (kernel == SPH_FORCE) ctx->stats.last_force_ms = b;
+    if (times) {
+      times->prologue_ns = (int64_t)(a * 1e6);
+      times->compute_ns = (int64_t)(b * 1e6);
+      times->epilogue_ns = (int64_t)(c * 1e6);
+    }
+    return SPH_OK;
+  });
+}
+
+int sph_run_sweep(sph_ctx *ctx, int kernel, void *const *recs, const sph_params *par, int path,
+                  int order, int guard, sph_times *times) {
+  (void)order;
+  (void)guard;
+  return guarded(ctx, [&] {
+    if (!ctx->bound) throw ArgError{"sph_run_sweep before sph_bind"};
+    if (!par) throw ArgError{"null params"};
+    check_kernel(kernel);
+    // Only the kernel's A_in crosses the bus on the way in and its A_out on the way back
+    // (the paper's map-direction rule, "only data in A_in has to be copied").
+    CK(cudaEventRecord(ctx->ev[4], ctx->stream));
+    ctx->upload_fields(recs, kernel_in(kernel) | F_FLAGS);
+    CK(cudaEventRecord(ctx->ev[5], ctx->stream));
+    ctx->sweep(kernel, to_params(par), path);
+    CK(cudaEventRecord(ctx->ev[6], ctx->stream));
+    ctx->download_fields(recs, kernel_out(kernel));
+    ctx->dirty = 0;
+    CK(cudaEventRecord(ctx->ev[7], ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    float a = 0, b = 0, c = 0;
+    CK(cudaEventElapsedTime(&a, ctx->ev[4], ctx->ev[5]));
+    CK(cudaEventElapsedTime(&b, ctx->ev[5], ctx->ev[6]));
+    CK(cudaEventElapsedTime(&c, ctx->ev[6], ctx->ev[7]));
+    if (times) {
+      times->prologue_ns = (int64_t)(a * 1e6);
+      times->compute_ns = (int64_t)(b * 1e6);
+      times->epilogue_ns = (int64_t)(c * 1e6);
+    }
+    return SPH_OK;
+  });
+}
+
+int sph_rebin(sph_ctx *ctx) {
+  return guarded(ctx, [&] {
+    if (!ctx->bound) throw ArgError{"sph_rebin before sph_bind"};
+    ctx->rebin();
+    CK(cudaStreamSynchronize(ctx->stream));
+    return SPH_OK;
+  });
+}
+
+int sph_step(sph_ctx *ctx, const sph_params *par, double *kernel_ms) {
+  return guarded(ctx, [&] {
+    if (!ctx->bound) throw ArgError{"sph_step before sph_bind"};
+    if (!par) throw ArgError{"null params"};
+    const Params p = to_params(par);
+    const int path = SPH_PATH_AOS_BASELINE;
+    cudaEvent_t *e = ctx->ev + 8;
+    CK(cudaEventRecord(e[0], ctx->stream));
+    ctx->sweep(SPH_KICK1, p, path);
+    CK(cudaEventRecord(e[1], ctx->stream));
+    ctx->sweep(SPH_DRIFT, p, path);
+    CK(cudaEventRecord(e[2], ctx->stream));
+    ctx->rebin();
+    CK(cudaEventRecord(e[3], ctx->stream));
+    ctx->sweep(SPH_DENSITY, p, path);
+    CK(cudaEventRecord(e[4], ctx->stream));
+    ctx->sweep(SPH_FORCE, p, path);
+    CK(cudaEventRecord(e[5], ctx->stream));
+    ctx->sweep(SPH_KICK2, p, path);
+    CK(cudaEventRecord(e[6], ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    float ms[6];
+    for (int k = 0; k < 6; ++k) CK(cudaEventElapsedTime(&ms[k], e[k], e[k + 1]));
+    ctx->stats.last_density_ms = ms[3];
+    ctx->stats.last_force_ms = ms[4];
+    if (kernel_ms)
+      for (int k = 0; k < 6; ++k) kernel_ms[k] = ms[k];
+    return SPH_OK;
+  });
+}
+
+int sph_make_particles(sph_ctx *ctx, int64_t n, int ppc, uint64_t seed, sph_params *par_out) {
+  return guarded(ctx, [&] {
+    if (ppc <= 0) throw ArgError{"ppc must be positive"};
+    n = std::max<int64_t>(n, 1);
+    if (n >= (1LL << 31)) throw ArgError{"n too large"};
+    // proto records in id order (grid.cpp:77-98)
+    Mt64 rng(seed);
+    const int nx = grid_nx(n, ppc);
+    const double cell_size = 1.0 / nx;
+    const double h_warm = 0.8 * cell_size / kSupport;
+    std::vector<Particle> proto((size_t)n);
+    std::vector<int> cell((size_t)n);
+    for (int64_t i = 0; i < n; ++i) {
+      Particle &p = proto[(size_t)i];
+      std::memset(&p, 0, sizeof p);
+      p.x[0] = rng.unit();
+      p.x[1] = rng.unit();
+      p.v[0] = (rng.unit() * 2.0 - 1.0) * 0.05;
+      p.v[1] = (rng.unit() * 2.0 - 1.0) * 0.05;
+      p.v_pred[0] = p.v[0];
+      p.v_pred[1] = p.v[1];
+      p.u = 0.5 + rng.unit();
+      p.u_pred = p.u;
+      p.m = 1.0 / static_cast<double>(n);
+      p.h = h_warm;
+      p.dt_next = 1.0e30;
+      p.id = i;
+      int cx = std::max(0, std::min((int)std::floor(p.x[0] * nx), nx - 1));
+      int cy = std::max(0, std::min((int)std::floor(p.x[1] * nx), nx - 1));
+      cell[(size_t)i] = cy * nx + cx;
+      p.cell = cell[(size_t)i]; // build_grid writes p->cell (grid.cpp:156)
+    }
+    // continuous store: sorted by (cell, id) (grid.cpp:117-132) == stable bucket by cell
+    const int nc = nx * nx;
+    std::vector<int64_t> cb((size_t)nc + 1, 0);
+    for (int64_t i = 0; i < n; ++i) cb[(size_t)cell[(size_t)i] + 1]++;
+    for (int c = 0; c < nc; ++c) cb[(size_t)c + 1] += cb[(size_t)c];
+    std::vector<int64_t> pos(cb.begin(), cb.end() - 1);
+    ctx->h_stage.ensure((size_t)n * sizeof(Particle));
+    Particle *sorted = static_cast<Particle *>(ctx->h_stage.p);
+    for (int64_t i = 0; i < n; ++i) sorted[pos[(size_t)cell[(size_t)i]]++] = proto[(size_t)i];
+    std::vector<Particle>().swap(proto);
+    std::vector<void *> ptrs((size_t)n);
+    for (int64_t k = 0; k < n; ++k) ptrs[(size_t)k] = sorted + k;
+    ctx->bind(ptrs.data(), cb.data(), nx, nx, cell_size, nullptr);
+
+    const int save_num = ctx->numerics, save_layout = ctx->layout;
+    ctx->numerics = SPH_NUMERICS_EXACT;
+    ctx->layout = SPH_LAYOUT_AOS;
+    Params p{1.0e-4, 5.0 / 3.0, 0.1, 1.0, 0.0};
+    // mean_wcount (grid.cpp:31-54): per-particle sums on the device, total in list order
+    ctx->wc.ensure(n);
+    ctx->run_density(true, true, p, true);
+    std::vector<double> wc((size_t)n);
+    CK(cudaMemcpyAsync(wc.data(), ctx->wc.p, sizeof(double) * n, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    double total = 0.0;
+    for (int64_t k = 0; k < n; ++k) total += wc[(size_t)k];
+    p.target_wcount = total / static_cast<double>(n);
+    ctx->sweep(SPH_DENSITY, p, SPH_PATH_AOS_BASELINE);
+    launch_eos(ctx->aos.p, (int)n, p.gamma, ctx->stream); // grid.cpp:137-140
+    ctx->launched();
+    ctx->sweep(SPH_FORCE, p, SPH_PATH_AOS_BASELINE);
+    CK(cudaStreamSynchronize(ctx->stream));
+    ctx->numerics = save_num;
+    ctx->layout = save_layout;
+    ctx->dirty = 0;
+    if (par_out) *par_out = sph_params{p.dt, p.gamma, p.cfl, p.grav, p.target_wcount};
+    return SPH_OK;
+  });
+}
+
+int sph_get_stats(const sph_ctx *ctx, sph_stats *out) {
+  if (!ctx || !out) return SPH_E_ARG;
+  *out = ctx->stats;
+  out->layout = ctx->layout;
+  out->numerics = ctx->numerics;
+  return SPH_OK;
+}
+
+int sph_synchronize(sph_ctx *ctx) {
+  return guarded(ctx, [&] {
+    CK(cudaStreamSynchronize(ctx->stream));
+    return SPH_OK;
+  });
+}
+
+int sph_fp64_peak(sph_ctx *ctx, double *tflops) {
+  return guarded(ctx, [&] {
+    int sms = 0;
+    CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device));
+    DevBuf<double> out;
+    out.ensure(1);
+    const int blocks = sms * 8, iters = 4096;
+    launch_fp64_probe(out.p, blocks, 64, ctx->stream); // warm-up
+    CK(cudaEventRecord(ctx->ev[0], ctx->stream));
+    launch_fp64_probe(out.p, blocks, iters, ctx->stream);
+    CK(cudaEventRecord(ctx->ev[1], ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    ctx->launched(2);
+    float ms = 0;
+    CK(cudaEventElapsedTime(&ms, ctx->ev[0], ctx->ev[1]));
+    out.release();
+    const double flops = 2.0 * 64.0 * 256.0 * (double)blocks * (double)iters;
+    if (tflops) *tflops = flops / (ms * 1e-3) / 1e12;
+    return SPH_OK;
+  });
+}
+
+int64_t sph_launch_count(const sph_ctx *ctx) { return ctx ? ctx->launches : 0; }
+
+} // extern "C"

@@ -1,0 +1,57 @@
+// sph_kernels.h — internal launcher declarations shared by the host runtime (capi.cu).
+#pragma once
+#include "sph_common.cuh"
+
+namespace sphb {
+
+struct DenArgs;
+struct ForArgs;
+
+// pair sweeps (pair_kernels.cuh instantiations)
+void launch_density_exact(const DenArgs &a, int n_items, bool aos, bool meanw, cudaStream_t s);
+void launch_force_exact(const ForArgs &a, int n_items, bool aos, cudaStream_t s);
+void launch_density_fast(const DenArgs &a, int n_items, bool aos, cudaStream_t s);
+void launch_force_fast(const ForArgs &a, int n_items, bool aos, cudaStream_t s);
+
+// streaming kernels (kernels_exact.cu); kernel = SPH_DRIFT / SPH_KICK1 / SPH_KICK2
+void launch_linear(int kernel, bool aos, Particle *p, const SoaMirror &f, int n, const Params &par,
+                   cudaStream_t s);
+void launch_eos(Particle *p, int n, double gamma, cudaStream_t s);
+
+// layout / bookkeeping kernels (kernels_layout.cu)
+// AoS -> SoA for the fields in `mask` (the paper's gather view) and SoA -> AoS scatter.
+void launch_gather(const Particle *aos, const SoaMirror &f, int n, uint32_t mask, cudaStream_t s);
+void launch_scatter(Particle *aos, const SoaMirror &f, int n, uint32_t mask, cudaStream_t s);
+// dense (host order) records -> device slots and back (full records)
+void launch_expand(Particle *aos, const Particle *dense, const int *host_idx, int n, cudaStream_t s);
+void launch_compact(Particle *dense, const Particle *aos, const int *host_idx, int n, cudaStream_t s);
+// pack / unpack selected fields between device slots and a dense per-field buffer in host order.
+// Buffer layout: for each field group in `mask` (ascending bit order) a block of n * size bytes.
+size_t packed_bytes_per_record(uint32_t mask);
+void launch_pack(char *dense, const Particle *aos, const int *host_idx, int n, uint32_t mask,
+                 cudaStream_t s);
+void launch_unpack_fields(Particle *aos, const char *dense, const int *host_idx, int n,
+                          uint32_t mask, cudaStream_t s);
+// spatial order of the locals within each cell (8x8 sub-cell bins); writes ilist
+void launch_spatial_order(int *ilist, const Particle *aos, const SoaMirror &f, bool aos_src,
+                          const int *cell_begin, int ncells, int nx, int ny, cudaStream_t s);
+// work items from per-cell counts: items for cell c cover list[cell_begin[c] + k*kTI ...];
+// out2[0] = n_items, out2[1] = pair count (sum cnt_c * na_c, int64 split in two ints)
+void launch_make_items(Item *items, int *n_items_out, long long *pairs_out, const int *cnt,
+                       const int *cell_begin, const int *na_cell, int ncells, cudaStream_t s);
+// per-cell active counts (sum of stencil cell counts) and per-cell local counts
+void launch_cell_counts(int *na_cell, int *cnt, const int *cell_begin, int nx, int ny,
+                        cudaStream_t s);
+// rebin helpers
+void launch_rebin_keys(unsigned long long *keys, int *vals, int *cellnew, const Particle *aos,
+                       const SoaMirror &f, bool aos_src, const long long *all_rank, int n, int nx,
+                       int ny, cudaStream_t s);
+void launch_cell_begin_from_sorted(int *cell_begin, const unsigned long long *keys, int n,
+                                   int ncells, cudaStream_t s);
+template <class T>
+void launch_permute(T *dst, const T *src, const int *perm, int n, cudaStream_t s);
+void launch_set_cell(Particle *aos, const int *cell_begin, int ncells, cudaStream_t s);
+// FP64 DFMA throughput probe
+void launch_fp64_probe(double *out, int blocks, int iters, cudaStream_t s);
+
+} // namespace sphb

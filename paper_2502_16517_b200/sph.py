@@ -1,0 +1,340 @@
+"""Host-side mirror of the reference SPH API, backed by the B200 C-ABI.
+
+Mirrors, with the same names, argument meaning and error behaviour:
+
+* ``ParticleStore`` / ``CellGrid`` / ``InitConfig``      (grid.hpp:17-47)
+* ``make_particles(cfg, par)``                           (grid.hpp:53, grid.cpp:76-143)
+* ``build_grid(store, cfg)``                             (grid.hpp:54, grid.cpp:145-184)
+* ``run_sweep(k, grid, par, path, order, guard, threads)`` (kernels.hpp:45-46)
+* ``update_count(grid)``, ``drift_one/kick1_one/kick2_one`` (kernels.hpp:49-54)
+
+Records live in one numpy array of the 272-byte ``PARTICLE_DTYPE``; ``store.all[k]`` is
+the record index of the k-th particle of ``ParticleStore::all``. ``run_sweep`` hands the
+flattened local lists to ``sph_run_sweep`` (upload of the kernel's A_in, sweep on the
+device, download of its A_out) — there is no CPU compute path.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _lib
+from .particle import (PARTICLE_DTYPE, RECORD_SIZE, DeviceLayout, Guard, KernelId, KernelTimes,
+                       Layout, Numerics, Order, Path, SphParams)
+
+
+def _check(ctx_handle, rc: int, what: str) -> None:
+    if rc != _lib.SPH_OK:
+        lib = _lib.load()
+        msg = lib.sph_last_error(ctx_handle) if ctx_handle else b"no context"
+        raise _lib.SphError(f"{what} failed ({rc}): {msg.decode(errors='replace')}")
+
+
+def _cpar(par: SphParams) -> _lib.SphParamsC:
+    return _lib.SphParamsC(par.dt, par.gamma, par.cfl, par.grav, par.target_wcount)
+
+
+@dataclass
+class InitConfig:
+    n: int = 1000
+    ppc: int = 64
+    seed: int = 42
+    layout: Layout = Layout.Scattered
+
+
+@dataclass
+class ParticleStore:
+    """Records + the ParticleStore::all order (record index of each particle)."""
+    recs: np.ndarray
+    all: np.ndarray
+    layout: Layout = Layout.Continuous
+
+    def size(self) -> int:
+        return len(self.all)
+
+    def snapshot(self) -> np.ndarray:
+        """Values of all particles in ``all`` order (grid.cpp:58-63)."""
+        return self.recs[self.all].copy()
+
+    def restore(self, snap: np.ndarray) -> None:
+        """Write values back, preserving storage positions (grid.cpp:65-67)."""
+        self.recs[self.all] = snap
+
+
+@dataclass
+class CellGrid:
+    """Uniform grid on [0,1)^2; local lists as CSR of record indices (grid.hpp:32-40).
+
+    The active list of a cell is the reference's deduplicated wrapped 3x3 stencil
+    (grid.cpp:159-182) and is implied by (nx, ny); ``active(c)`` materialises it."""
+    nx: int
+    ny: int
+    cell_size: float
+    cell_begin: np.ndarray          # int64[ncells + 1]
+    local_idx: np.ndarray           # int64[n], record indices, cell-major
+    store: ParticleStore
+    all_rank: np.ndarray = field(default=None)  # rank in store.all of each local entry
+
+    def cells(self) -> int:
+        return self.nx * self.ny
+
+    def mean_ppc(self) -> float:
+        return float(self.cell_begin[-1]) / self.cells() if self.cells() else 0.0
+
+    def local(self, c: int) -> np.ndarray:
+        return self.local_idx[self.cell_begin[c]:self.cell_begin[c + 1]]
+
+    def stencil(self, c: int) -> list[int]:
+        cy, cx = divmod(c, self.nx)
+        out: list[int] = []
+        for dy in (-1, 0, 1):
+            for dx in (-1, 0, 1):
+                ci = ((cy + dy) % self.ny) * self.nx + (cx + dx) % self.nx
+                if ci not in out:
+                    out.append(ci)
+        return out
+
+    def active(self, c: int) -> np.ndarray:
+        return np.concatenate([self.local(k) for k in self.stencil(c)])
+
+    def record_pointers(self) -> np.ndarray:
+        """Particle* of every local entry (the flattened CellGrid::local)."""
+        base = self.store.recs.ctypes.data
+        return (base + self.local_idx * RECORD_SIZE).astype(np.uint64)
+
+
+def grid_nx(n: int, ppc: int) -> int:
+    """grid.cpp:23-26."""
+    cell = np.sqrt(float(ppc) / float(max(n, 1)))
+    return max(1, int(np.floor(1.0 / cell)))
+
+
+def build_grid(store: ParticleStore, cfg: InitConfig) -> CellGrid:
+    """build_grid (grid.cpp:145-184): cell = clamp(floor(x*nx)), lists in ``all`` order.
+
+    Writes each record's ``cell`` like the reference (grid.cpp:156)."""
+    nx = grid_nx(store.size(), cfg.ppc)
+    ny = nx
+    x = store.recs["x"][store.all]
+    cx = np.clip(np.floor(x[:, 0] * nx).astype(np.int64), 0, nx - 1)
+    cy = np.clip(np.floor(x[:, 1] * nx).astype(np.int64), 0, ny - 1)
+    ci = cy * nx + cx
+    store.recs["cell"][store.all] = ci
+    order = np.argsort(ci, kind="stable")              # stable: keeps ``all`` order per cell
+    cb = np.zeros(nx * ny + 1, np.int64)
+    np.cumsum(np.bincount(ci, minlength=nx * ny), out=cb[1:])
+    return CellGrid(nx, ny, 1.0 / nx, cb, store.all[order].astype(np.int64), store,
+                    all_rank=order.astype(np.int64))
+
+
+def update_count(grid: CellGrid) -> int:
+    """kernels.cpp:874-878."""
+    return int(grid.cell_begin[-1])
+
+
+class Context:
+    """One device context (CUDA stream + device mirror of one bound grid)."""
+
+    def __init__(self, device: int = 0, numerics: Numerics = Numerics.Fast,
+                 layout: DeviceLayout = DeviceLayout.FromPath):
+        self.lib = _lib.load()
+        h = C.c_void_p()
+        rc = self.lib.sph_create(device, C.byref(h))
+        if rc != _lib.SPH_OK:
+            raise _lib.SphError(f"sph_create(device={device}) failed ({rc}): no usable CUDA device")
+        self.h = h.value
+        self.grid: CellGrid | None = None
+        self._ptrs: np.ndarray | None = None
+        self.set_numerics(numerics)
+        self.set_layout(layout)
+
+    # -- configuration --
+    def set_numerics(self, numerics: Numerics) -> None:
+        _check(self.h, self.lib.sph_set_numerics(self.h, int(numerics)), "sph_set_numerics")
+        self.numerics = Numerics(numerics)
+
+    def set_layout(self, layout: DeviceLayout) -> None:
+        _check(self.h, self.lib.sph_set_layout(self.h, int(layout)), "sph_set_layout")
+        self.layout = DeviceLayout(layout)
+
+    # -- binding / transfers --
+    def bind(self, grid: CellGrid) -> None:
+        ptrs = grid.record_pointers()
+        cb = np.ascontiguousarray(grid.cell_begin, np.int64)
+        rank = None if grid.all_rank is None else np.ascontiguousarray(grid.all_rank, np.int64)
+        rc = self.lib.sph_bind(self.h, ptrs.ctypes.data, cb.ctypes.data, grid.nx, grid.ny,
+                               grid.cell_size, None if rank is None else rank.ctypes.data)
+        _check(self.h, rc, "sph_bind")
+        self.grid, self._ptrs, self._rank = grid, ptrs, rank
+
+    def _need(self) -> None:
+        if self.grid is None:
+            raise _lib.SphError("context has no bound grid")
+
+    def upload(self) -> None:
+        self._need()
+        _check(self.h, self.lib.sph_upload(self.h, self._ptrs.ctypes.data), "sph_upload")
+
+    def download(self) -> None:
+        self._need()
+        _check(self.h, self.lib.sph_download(self.h, self._ptrs.ctypes.data), "sph_download")
+
+    def download_all(self) -> None:
+        self._need()
+        _check(self.h, self.lib.sph_download_all(self.h, self._ptrs.ctypes.data), "sph_download_all")
+
+    # -- compute --
+    def sweep(self, k: KernelId, par: SphParams, path: Path = Path.AosBaseline,
+              order: Order = Order.LocalActive, guard: Guard = Guard.Branch) -> KernelTimes:
+        self._need()
+        t = _lib.SphTimesC()
+        cp = _cpar(par)
+        _check(self.h, self.lib.sph_sweep(self.h, int(k), C.byref(cp), int(path), int(order),
+                                          int(guard), C.byref(t)), "sph_sweep")
+        return KernelTimes(t.prologue_ns, t.compute_ns, t.epilogue_ns)
+
+    def run_sweep(self, k: KernelId, par: SphParams, path: Path = Path.AosBaseline,
+                  order: Order = Order.LocalActive, guard: Guard = Guard.Branch) -> KernelTimes:
+        self._need()
+        t = _lib.SphTimesC()
+        cp = _cpar(par)
+        _check(self.h, self.lib.sph_run_sweep(self.h, int(k), self._ptrs.ctypes.data, C.byref(cp),
+                                              int(path), int(order), int(guard), C.byref(t)),
+               "sph_run_sweep")
+        return KernelTimes(t.prologue_ns, t.compute_ns, t.epilogue_ns)
+
+    def rebin(self) -> None:
+        self._need()
+        _check(self.h, self.lib.sph_rebin(self.h), "sph_rebin")
+
+    def step(self, par: SphParams) -> np.ndarray:
+        """kick1 -> drift -> rebin -> density -> force -> kick2 on the device; per-phase ms."""
+        self._need()
+        ms = np.zeros(6, np.float64)
+        cp = _cpar(par)
+        _check(self.h, self.lib.sph_step(self.h, C.byref(cp), ms.ctypes.data), "sph_step")
+        return ms
+
+    def make_particles(self, n: int, ppc: int, seed: int) -> tuple[ParticleStore, CellGrid, SphParams]:
+        """The reference IC computed on the device and left bound (continuous store)."""
+        cp = _lib.SphParamsC()
+        _check(self.h, self.lib.sph_make_particles(self.h, n, ppc, seed, C.byref(cp)),
+               "sph_make_particles")
+        n = max(n, 1)
+        recs = np.zeros(n, PARTICLE_DTYPE)
+        _check(self.h, self.lib.sph_read_records(self.h, recs.ctypes.data), "sph_read_records")
+        store = ParticleStore(recs, np.arange(n, dtype=np.int64), Layout.Continuous)
+        grid = build_grid(store, InitConfig(n=n, ppc=ppc, seed=seed, layout=Layout.Continuous))
+        self.grid = grid
+        self._ptrs = grid.record_pointers()
+        return store, grid, SphParams(cp.dt, cp.gamma, cp.cfl, cp.grav, cp.target_wcount)
+
+    def read_records(self) -> np.ndarray:
+        self._need()
+        out = np.zeros(len(self._ptrs), PARTICLE_DTYPE)
+        _check(self.h, self.lib.sph_read_records(self.h, out.ctypes.data), "sph_read_records")
+        return out
+
+    def stats(self) -> dict:
+        s = _lib.SphStatsC()
+        _check(self.h, self.lib.sph_get_stats(self.h, C.byref(s)), "sph_get_stats")
+        return {name: getattr(s, name) for name, _ in s._fields_ if name != "pad0"}
+
+    def fp64_peak_tflops(self) -> float:
+        v = C.c_double()
+        _check(self.h, self.lib.sph_fp64_peak(self.h, C.byref(v)), "sph_fp64_peak")
+        return v.value
+
+    def launch_count(self) -> int:
+        return int(self.lib.sph_launch_count(self.h))
+
+    def synchronize(self) -> None:
+        _check(self.h, self.lib.sph_synchronize(self.h), "sph_synchronize")
+
+    def close(self) -> None:
+        if getattr(self, "h", None):
+            self.lib.sph_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+
+_default: Context | None = None
+
+
+def default_context() -> Context:
+    global _default
+    if _default is None:
+        _default = Context(0)
+    return _default
+
+
+def make_particles(cfg: InitConfig, par: SphParams, ctx: Context | None = None) -> ParticleStore:
+    """make_particles (grid.cpp:76-143): deterministic IC; calibrates par.target_wcount.
+
+    The density / EOS / force initialisation passes run on the device with EXACT numerics,
+    so the records are byte-identical to the reference's."""
+    ctx = ctx or default_context()
+    store, _, p = ctx.make_particles(cfg.n, cfg.ppc, cfg.seed)
+    par.dt, par.gamma, par.cfl, par.grav, par.target_wcount = p.dt, p.gamma, p.cfl, p.grav, p.target_wcount
+    if cfg.layout == Layout.Scattered:
+        # values are layout-independent (test_sph.cpp:138-149); store them by id
+        ids = store.recs["id"]
+        recs = np.empty_like(store.recs)
+        recs[ids] = store.recs
+        store = ParticleStore(recs, np.arange(len(recs), dtype=np.int64), Layout.Scattered)
+    return store
+
+
+def run_sweep(k: KernelId, grid: CellGrid, par: SphParams, path: Path = Path.AosBaseline,
+              order: Order = Order.LocalActive, guard: Guard = Guard.Branch, threads: int = 1,
+              ctx: Context | None = None) -> KernelTimes:
+    """Drop-in for soaview::sph::run_sweep (kernels.hpp:45-46) on the B200.
+
+    ``threads`` is accepted for signature parity; the device decides its own parallelism.
+    Path selects the device layout (AosBaseline: AoS in place, SoaView: per-call AoS->SoA
+    conversion) unless the context forces one."""
+    ctx = ctx or default_context()
+    if ctx.grid is not grid:
+        ctx.bind(grid)
+    return ctx.run_sweep(k, par, path, order, guard)
+
+
+# Single-particle ops (kernels.hpp:52-54) run as a one-particle sweep on the device.
+def _one(kernel: KernelId, rec: np.ndarray, par: SphParams, ctx: Context | None) -> None:
+    """``rec``: a one-element PARTICLE_DTYPE array (e.g. ``recs[i:i+1]``), updated in place."""
+    ctx = ctx or default_context()
+    one = np.asarray(rec)
+    if one.dtype != PARTICLE_DTYPE or one.size != 1 or not one.flags.c_contiguous:
+        raise ValueError("expected a contiguous one-element PARTICLE_DTYPE array view")
+    one = one.reshape(1)
+    store = ParticleStore(one, np.zeros(1, np.int64), Layout.Continuous)
+    grid = CellGrid(1, 1, 1.0, np.array([0, 1], np.int64), np.zeros(1, np.int64), store,
+                    all_rank=np.zeros(1, np.int64))
+    ctx.bind(grid)
+    ctx.run_sweep(kernel, par)
+    ctx.grid = None
+
+
+def drift_one(rec: np.ndarray, par: SphParams, ctx: Context | None = None) -> None:
+    _one(KernelId.Drift, rec, par, ctx)
+
+
+def kick1_one(rec: np.ndarray, par: SphParams, ctx: Context | None = None) -> None:
+    _one(KernelId.Kick1, rec, par, ctx)
+
+
+def kick2_one(rec: np.ndarray, par: SphParams, ctx: Context | None = None) -> None:
+    _one(KernelId.Kick2, rec, par, ctx)
