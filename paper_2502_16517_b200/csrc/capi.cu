@@ -473,8 +473,7 @@ struct sph_ctx {
   size_t download_fields(void *const *recs, uint32_t mask) {
     if (n == 0 || !mask) return 0;
     make_aos_current();
-    const size_t per = packed_bytes_per_record(mask);
-    const size_t bytes = per * (size_t)n;
+    const size_t bytes = packed_bytes(mask, (size_t)n);
     dense.ensure(bytes);
     h_stage.ensure(bytes);
     launch_pack(dense.p, aos.p, host_idx.p, (int)n, mask, stream);
@@ -488,7 +487,7 @@ struct sph_ctx {
     for (const HostField &f : kHostFields)
       if (mask & f.bit) {
         fl.push_back({f, base});
-        base += (size_t)f.size * (size_t)n;
+        base += ((size_t)f.size * (size_t)n + 15) & ~(size_t)15;
       }
     parallel_for(n, [&](int64_t b, int64_t e) {
       for (int64_t k = b; k < e; ++k) {
@@ -651,7 +650,7 @@ size_t sph_ctx::upload_fields(void *const *recs, uint32_t mask) {
   for (const HostField &f : kHostFields)
     if (mask & f.bit) {
       fl.push_back({f, base});
-      base += (size_t)f.size * (size_t)n;
+      base += ((size_t)f.size * (size_t)n + 15) & ~(size_t)15;
     }
   h_stage.ensure(base);
   char *st = static_cast<char *>(h_stage.p);

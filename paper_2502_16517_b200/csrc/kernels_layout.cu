@@ -127,10 +127,13 @@ __global__ void pack_kernel(char *__restrict__ dense, const Particle *__restrict
     const FieldDesc fd = c_fields[k];
     if (!(mask & fd.bit)) continue;
     char *dst = dense + base + h * fd.size;
-    if (fd.size == 16) *reinterpret_cast<uint4 *>(dst) = *reinterpret_cast<const uint4 *>(rec + fd.offset);
-    else if (fd.size == 8) *reinterpret_cast<unsigned long long *>(dst) = *reinterpret_cast<const unsigned long long *>(rec + fd.offset);
+    // 16-byte fields move as two 8-byte words: dbg[2] sits at offset 216, 8-aligned only
+    if (fd.size == 16) {
+      reinterpret_cast<unsigned long long *>(dst)[0] = reinterpret_cast<const unsigned long long *>(rec + fd.offset)[0];
+      reinterpret_cast<unsigned long long *>(dst)[1] = reinterpret_cast<const unsigned long long *>(rec + fd.offset)[1];
+    } else if (fd.size == 8) *reinterpret_cast<unsigned long long *>(dst) = *reinterpret_cast<const unsigned long long *>(rec + fd.offset);
     else *reinterpret_cast<unsigned *>(dst) = *reinterpret_cast<const unsigned *>(rec + fd.offset);
-    base += (long long)n * fd.size;
+    base += ((long long)n * fd.size + 15) & ~15LL; // 16-byte aligned field blocks
   }
 }
 
@@ -145,10 +148,12 @@ __global__ void unpack_kernel(Particle *__restrict__ aos, const char *__restrict
     const FieldDesc fd = c_fields[k];
     if (!(mask & fd.bit)) continue;
     const char *src = dense + base + h * fd.size;
-    if (fd.size == 16) *reinterpret_cast<uint4 *>(rec + fd.offset) = *reinterpret_cast<const uint4 *>(src);
-    else if (fd.size == 8) *reinterpret_cast<unsigned long long *>(rec + fd.offset) = *reinterpret_cast<const unsigned long long *>(src);
+    if (fd.size == 16) {
+      reinterpret_cast<unsigned long long *>(rec + fd.offset)[0] = reinterpret_cast<const unsigned long long *>(src)[0];
+      reinterpret_cast<unsigned long long *>(rec + fd.offset)[1] = reinterpret_cast<const unsigned long long *>(src)[1];
+    } else if (fd.size == 8) *reinterpret_cast<unsigned long long *>(rec + fd.offset) = *reinterpret_cast<const unsigned long long *>(src);
     else *reinterpret_cast<unsigned *>(rec + fd.offset) = *reinterpret_cast<const unsigned *>(src);
-    base += (long long)n * fd.size;
+    base += ((long long)n * fd.size + 15) & ~15LL; // 16-byte aligned field blocks
   }
 }
 
@@ -318,10 +323,10 @@ int grid_for(long long total, int block) {
 
 } // namespace
 
-size_t packed_bytes_per_record(uint32_t mask) {
+size_t packed_bytes(uint32_t mask, size_t n) {
   size_t b = 0;
   for (int k = 0; k < kNumFields; ++k)
-    if (mask & h_fields[k].bit) b += (size_t)h_fields[k].size;
+    if (mask & h_fields[k].bit) b += ((size_t)h_fields[k].size * n + 15) & ~(size_t)15;
   return b;
 }
 

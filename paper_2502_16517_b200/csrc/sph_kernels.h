@@ -26,8 +26,9 @@ void launch_scatter(Particle *aos, const SoaMirror &f, int n, uint32_t mask, cud
 void launch_expand(Particle *aos, const Particle *dense, const int *host_idx, int n, cudaStream_t s);
 void launch_compact(Particle *dense, const Particle *aos, const int *host_idx, int n, cudaStream_t s);
 // pack / unpack selected fields between device slots and a dense per-field buffer in host order.
-// Buffer layout: for each field group in `mask` (ascending bit order) a block of n * size bytes.
-size_t packed_bytes_per_record(uint32_t mask);
+// Buffer layout: for each field group in `mask` (ascending bit order) a block of n * size
+// bytes, each block starting 16-byte aligned.
+size_t packed_bytes(uint32_t mask, size_t n);
 void launch_pack(char *dense, const Particle *aos, const int *host_idx, int n, uint32_t mask,
                  cudaStream_t s);
 void launch_unpack_fields(Particle *aos, const char *dense, const int *host_idx, int n,
