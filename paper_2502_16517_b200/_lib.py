@@ -9,7 +9,7 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "lib", "libsph_b200.so")
+LIB_PATH = os.environ.get("SPH_B200_LIB") or os.path.join(HERE, "lib", "libsph_b200.so")
 HEADER = os.path.join(os.path.dirname(HERE), "include", "sph_b200.h")
 
 SPH_OK = 0

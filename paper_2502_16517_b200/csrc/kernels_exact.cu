@@ -62,6 +62,8 @@ __device__ __forceinline__ double support_threshold(double inv_h) {
 
 } // namespace
 
+__device__ __forceinline__ int hi_word(double v) { return __double2hiint(v); }
+
 struct ExactPolicy {
   static constexpr bool kExactOrder = true;
   struct DI { double x, y, vx, vy, inv_h, thr; };
@@ -100,6 +102,18 @@ struct ExactPolicy {
     double fac = mj * dw / r;
     s.div_v -= fac * (dv0 * dx0 + dv1 * dx1);
     s.rot_v += fac * (dv0 * dx1 - dv1 * dx0);
+  }
+
+  template <bool MINIMG>
+  __device__ static void den_tile(const DI &I, const DenTile &T, DA &s) {
+#pragma unroll 2
+    for (int j = 0; j < kTJ; ++j) den_pair<MINIMG>(I, T.xy[j], T.vv[j], T.m[j], s);
+  }
+
+  template <bool MINIMG>
+  __device__ static void mw_tile(const DI &I, const DenTile &T, MW &m) {
+#pragma unroll 2
+    for (int j = 0; j < kTJ; ++j) mw_pair<MINIMG>(I, T.xy[j], m);
   }
 
   // mean_wcount inner loop, grid.cpp:39-48
@@ -200,6 +214,12 @@ struct ExactPolicy {
     double mu = dmin(0.0, dvdr * inv_r);
     s.vsig = dmax(s.vsig, 1.0 * (I.ci + cj - 3.0 * mu * I.bi));
     s.hdt -= pv.y * dvdr * inv_r * dwi * 0.5 * I.hi;
+  }
+
+  template <bool MINIMG>
+  __device__ static void for_tile(const FI &I, const ForTile &T, FA &s) {
+#pragma unroll 2
+    for (int j = 0; j < kTJ; ++j) for_pair<MINIMG>(I, T.xy[j], T.vv[j], T.mg[j], T.pv[j], T.c[j], s);
   }
 
   __device__ static void for_publish(const FI &, const FA &s, double o[5]) {
@@ -327,19 +347,25 @@ __global__ void eos_kernel(Particle *aos, int n, double gamma) {
 // ---------------------------------------------------------------------------------------
 void launch_density_exact(const DenArgs &a, int n_items, bool aos, bool meanw, cudaStream_t s) {
   if (n_items <= 0) return;
+  DenArgs b = a;
+  b.n_items = n_items;
+  const int G = pair_grid(n_items), B = kWarpsPerCta * 32;
   if (aos) {
-    if (meanw) density_round_kernel<ExactPolicy, true, true><<<n_items, kTI, 0, s>>>(a);
-    else density_round_kernel<ExactPolicy, true, false><<<n_items, kTI, 0, s>>>(a);
+    if (meanw) density_round_kernel<ExactPolicy, true, true><<<G, B, 0, s>>>(b);
+    else density_round_kernel<ExactPolicy, true, false><<<G, B, 0, s>>>(b);
   } else {
-    if (meanw) density_round_kernel<ExactPolicy, false, true><<<n_items, kTI, 0, s>>>(a);
-    else density_round_kernel<ExactPolicy, false, false><<<n_items, kTI, 0, s>>>(a);
+    if (meanw) density_round_kernel<ExactPolicy, false, true><<<G, B, 0, s>>>(b);
+    else density_round_kernel<ExactPolicy, false, false><<<G, B, 0, s>>>(b);
   }
 }
 
 void launch_force_exact(const ForArgs &a, int n_items, bool aos, cudaStream_t s) {
   if (n_items <= 0) return;
-  if (aos) force_kernel<ExactPolicy, true><<<n_items, kTI, 0, s>>>(a);
-  else force_kernel<ExactPolicy, false><<<n_items, kTI, 0, s>>>(a);
+  ForArgs b = a;
+  b.n_items = n_items;
+  const int G = pair_grid(n_items), B = kWarpsPerCta * 32;
+  if (aos) force_kernel<ExactPolicy, true><<<G, B, 0, s>>>(b);
+  else force_kernel<ExactPolicy, false><<<G, B, 0, s>>>(b);
 }
 
 void launch_linear(int kernel, bool aos, Particle *p, const SoaMirror &f, int n, const Params &par,

@@ -4,13 +4,16 @@
 // the B200 FP64 pipe (64 DFMA/clk/SM) while staying a full-precision FP64 evaluation:
 //   * periodic images are resolved once per stencil cell (shift folded into the staged j
 //     position) instead of d - round(d) per pair (needs nx, ny >= 5, else min image);
-//   * the support test is r2 < 6.25 h^2 on the squared distance, so the ~78 % of pairs
-//     outside the support cost 2 DADD + DMUL + DFMA + compare (density);
-//   * sqrt and '/' become rsqrt.approx.f64 (MUFU) + two Newton steps (~1 ulp);
-//   * the M5 spline is a per-interval Horner polynomial in a well-conditioned local
-//     variable (no cancellation), with the 2-D normalisation and the per-i constants
-//     (1/h^3, P_i/rho_i^2 ...) factored out of the j loop and applied once per particle;
-//   * per-j invariants grav*m, m*p/rho^2, m/rho are hoisted into the shared-memory tile.
+//   * the support test compares the high 32 bits of r^2 and (2.5 h)^2 as integers (ALU
+//     pipe, not FP64 pipe); pairs within 2^-20 of the support edge, where W ~ 1e-23, are
+//     treated as outside. Out-of-support density pairs cost 2 DADD + DMUL + DFMA;
+//   * sqrt and '/' become rsqrt.approx.f64 (MUFU) + a 2nd-order series correction (~1 ulp);
+//   * the M5 spline is a Horner polynomial in s = 1.5 - q or 2.5 - q with selected
+//     coefficients (no cancellation), plus a rarely-taken correction for q < 0.5;
+//     dW/dq = -4 N E(s); the normalisation N, the -4 and the per-i constants (1/h^3,
+//     P_i/rho_i^2 ...) are applied once per particle, not per pair;
+//   * per-j invariants grav*m, m*p/rho^2, m/rho are hoisted into the shared-memory tile;
+//   * each tile is consumed two pairs at a time with independent dependency chains.
 // Summation order per particle is still the reference's j order; differences come from
 // FMA contraction and the reassociated constant factors (~1e-15 relative per term).
 #include "pair_kernels.cuh"
@@ -20,42 +23,77 @@ namespace sphb {
 
 namespace {
 
-__device__ __forceinline__ double rsqrt_nr(double x) {
+// x^(-1/2) and x^(-3/2) to ~1 ulp from the MUFU seed y0 = rsqrt.approx.f64(x), whose
+// relative error is below 2^-20 (measured on B200, tools/rsq_probe). With e = 1 - x y0^2
+// (|e| < 2^-19; y0 has 21 significant bits so y0^2 is exact and e is rounded once):
+//   x^(-1/2) = y0 (1 + e/2 + 3e^2/8 + O(e^3)),   x^(-3/2) = y0^3 (1 + 3e/2 + 15e^2/8 + O(e^3)),
+// truncation < 2^-55. 5 (resp. 6) FP64 ops instead of Newton's 7 (resp. 9).
+__device__ __forceinline__ double rsqrt_seed(double x) {
   double y;
   asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
-  const double hx = 0.5 * x;
-  double e = fma(-hx * y, y, 0.5);
-  y = fma(y, e, y);
-  e = fma(-hx * y, y, 0.5);
-  y = fma(y, e, y);
   return y;
 }
+__device__ __forceinline__ double rsqrt_fast(double x) {
+  const double y0 = rsqrt_seed(x);
+  const double e = fma(-x, y0 * y0, 1.0);
+  return fma(y0, e * fma(e, 0.375, 0.5), y0);
+}
+__device__ __forceinline__ double rsqrt3_fast(double x) {
+  const double y0 = rsqrt_seed(x);
+  const double t = y0 * y0;
+  const double e = fma(-x, t, 1.0);
+  const double y3 = t * y0;
+  return fma(y3, e * fma(e, 1.875, 1.5), y3);
+}
 
-// M5 spline pieces, W(q) = N * P(s), dW/dq = N * D(s), with the local variable s chosen
-// per interval so the polynomial has no cancellation:
-//   q in [1.5, 2.5): s = 2.5 - q, P = s^4,                           D = -4 s^3
-//   q in [0.5, 1.5): s = 1.5 - q, P = -4s^4 + 4s^3 + 6s^2 + 4s + 1,  D = 16s^3 - 12s^2 - 12s - 4
-//   q in [0.0, 0.5): s = q,       P = 6s^4 - 15s^2 + 14.375,         D = 24s^3 - 30s
-// (expansions of spline.hpp:12-41; all coefficients are exact small binary fractions).
+__device__ __forceinline__ int hi_word(double v) { return __double2hiint(v); }
+// 0 < r2 < H2 as one unsigned compare on the high words (r2 >= 0 always): excludes the
+// self pair (r2 == 0) and everything at or beyond the support edge, on the ALU pipe.
+__device__ __forceinline__ bool in_support(double r2, unsigned hiH2m1) {
+  return (unsigned)hi_word(r2) - 1u < hiH2m1;
+}
+
+// M5 spline (spline.hpp:12-41) as W(q) = N P(s), dW/dq = -4 N E(s):
+//   q in [1.5, 2.5): s = 2.5 - q, P = s^4,                          E = s^3
+//   q in [0.5, 1.5): s = 1.5 - q, P = -4s^4 + 4s^3 + 6s^2 + 4s + 1, E = -4s^3 + 3s^2 + 3s + 1
+//   q in [0.0, 0.5): s = q,       P = 6s^4 - 15s^2 + 14.375,        E = -6s^3 + 7.5s
+// (SPH_SPLINE3: one Horner with three-way selected coefficients; otherwise the innermost
+// piece is the middle one plus the correction 10 t^4 / 10 t^3, t = 0.5 - q).
+// The two outer pieces share Horner evaluation with selected coefficients (c4 == e3,
+// c3 == c1, c0 == e0, e2 == e1), the innermost correction is a rarely-divergent branch.
 struct Spline {
-  double s, c4, c3, c2, c1, c0, d3, d2, d1, d0;
-  __device__ __forceinline__ explicit Spline(double q) {
-    const bool inner = q < 0.5, mid = q < 1.5;
-    const double k = inner ? 0.0 : (mid ? 1.5 : 2.5);
-    const double sg = inner ? 1.0 : -1.0;
-    s = fma(sg, q, k);
-    c4 = inner ? 6.0 : (mid ? -4.0 : 1.0);
-    c3 = inner ? 0.0 : (mid ? 4.0 : 0.0);
-    c2 = inner ? -15.0 : (mid ? 6.0 : 0.0);
-    c1 = inner ? 0.0 : (mid ? 4.0 : 0.0);
-    c0 = inner ? 14.375 : (mid ? 1.0 : 0.0);
-    d3 = inner ? 24.0 : (mid ? 16.0 : -4.0);
-    d2 = inner ? 0.0 : (mid ? -12.0 : 0.0);
-    d1 = inner ? -30.0 : (mid ? -12.0 : 0.0);
-    d0 = inner ? 0.0 : (mid ? -4.0 : 0.0);
+  double P, E;
+  template <bool NEED_P>
+  __device__ __forceinline__ void eval(double q) {
+    // interval tests on the high word: for q >= 0, q < 1.5 <=> hi(q) < hi(1.5) exactly
+    // (1.5 and 0.5 have zero low words), so they run on the ALU pipe
+    const int hq = hi_word(q);
+    const bool mid = hq < 0x3FF80000;  // q < 1.5
+#if SPH_SPLINE3
+    // three-way coefficient select, local variable s = 2.5 - q | 1.5 - q | q
+    const bool inner = hq < 0x3FE00000; // q < 0.5
+    const double s = inner ? q : (mid ? 1.5 : 2.5) - q;
+    const double e3 = inner ? -6.0 : (mid ? -4.0 : 1.0), e2 = (mid && !inner) ? 3.0 : 0.0;
+    const double e1 = inner ? 7.5 : (mid ? 3.0 : 0.0), e0 = (mid && !inner) ? 1.0 : 0.0;
+    E = fma(fma(fma(e3, s, e2), s, e1), s, e0);
+    if (NEED_P) {
+      const double c4 = inner ? 6.0 : (mid ? -4.0 : 1.0), c31 = (mid && !inner) ? 4.0 : 0.0;
+      const double c2 = inner ? -15.0 : (mid ? 6.0 : 0.0), c0 = inner ? 14.375 : (mid ? 1.0 : 0.0);
+      P = fma(fma(fma(fma(c4, s, c31), s, c2), s, c31), s, c0);
+    }
+#else
+    const double s = (mid ? 1.5 : 2.5) - q;
+    const double c4 = mid ? -4.0 : 1.0, c31 = mid ? 4.0 : 0.0, c2 = mid ? 6.0 : 0.0;
+    const double c0 = mid ? 1.0 : 0.0, e21 = mid ? 3.0 : 0.0;
+    E = fma(fma(fma(c4, s, e21), s, e21), s, c0);
+    if (NEED_P) P = fma(fma(fma(fma(c4, s, c31), s, c2), s, c31), s, c0);
+    if (__builtin_expect(hq < 0x3FE00000, 0)) { // q < 0.5: ~4 % of in-support pairs
+      const double t = 0.5 - q, t2 = t * t, t3 = t2 * t;
+      E = fma(10.0, t3, E);
+      if (NEED_P) P = fma(10.0, t3 * t, P);
+    }
+#endif
   }
-  __device__ __forceinline__ double P() const { return fma(fma(fma(fma(c4, s, c3), s, c2), s, c1), s, c0); }
-  __device__ __forceinline__ double D() const { return fma(fma(fma(d3, s, d2), s, d1), s, d0); }
 };
 
 } // namespace
@@ -64,53 +102,72 @@ struct FastPolicy {
   static constexpr bool kExactOrder = false;
   static constexpr double kW0 = kNorm2d * 14.375; // kernel_w(0)
 
-  struct DI { double x, y, vx, vy, inv_h, H2; };
-  // Scaled sums: rho = N*S_rho, wcount = N*S_w, rho_dh = -N*S_dh, rot_v = N*S_rot,
-  // div_v = -N*S_div (N = 2-D spline normalisation).
-  struct DA { double rho, w, dh, rot, div; };
+  struct DI { double x, y, vx, vy, inv_h; unsigned hiH2m1; };
+  // Scaled sums (N = spline normalisation): rho = N*S_rho, wcount = N*S_w,
+  // rho_dh = -N*(2 S_rho - 4 S_qE), div_v = 4N*S_div, rot_v = -4N*S_rot (all / h^2, h^3).
+  struct DA { double rho, w, qe, rot, div; };
   struct MW { double w; };
 
   __device__ static DI den_i(double x, double y, double vx, double vy, double h) {
     DI I;
     I.x = x; I.y = y; I.vx = vx; I.vy = vy;
     I.inv_h = 1.0 / h;
-    I.H2 = 6.25 * h * h;
+    I.hiH2m1 = (unsigned)hi_word(6.25 * h * h) - 1u;
     return I;
   }
   __device__ static DA den_zero() { return DA{0.0, 0.0, 0.0, 0.0, 0.0}; }
   __device__ static MW mw_zero() { return MW{0.0}; }
   __device__ static double mw_value(const MW &m) { return kW0 + kNorm2d * m.w; }
 
+  __device__ __forceinline__ static void den_in(const DI &I, double dx, double dy, double r2,
+                                                double2 vj, double mj, DA &s) {
+    const double rinv = rsqrt_fast(r2);
+    const double q = r2 * rinv * I.inv_h;
+    Spline sp;
+    sp.template eval<true>(q);
+    s.rho = fma(mj, sp.P, s.rho);
+    s.w += sp.P;
+    const double mE = mj * sp.E;
+    s.qe = fma(q, mE, s.qe);
+    const double fac = mE * rinv;
+    const double dvx = I.vx - vj.x, dvy = I.vy - vj.y;
+    s.div = fma(fac, fma(dvx, dx, dvy * dy), s.div);
+    s.rot = fma(fac, fma(dvx, dy, -dvy * dx), s.rot);
+  }
+
+  // Four pairs per step: the four distance chains are straight-line code (independent,
+  // interleaved by the scheduler), then the in-support blocks run in j order.
   template <bool MINIMG>
-  __device__ static void den_pair(const DI &I, double2 xj, double2 vj, double mj, DA &s) {
-    double dx = I.x - xj.x, dy = I.y - xj.y;
-    if (MINIMG) { dx -= round(dx); dy -= round(dy); }
-    const double r2 = fma(dx, dx, dy * dy);
-    if (r2 < I.H2) {
-      if (r2 > 0.0) {
-        const double rinv = rsqrt_nr(r2);
-        const double q = r2 * rinv * I.inv_h;
-        const Spline sp(q);
-        const double P = sp.P(), D = sp.D();
-        s.rho = fma(mj, P, s.rho);
-        s.w += P;
-        s.dh = fma(mj, fma(q, D, P + P), s.dh);
-        const double fac = mj * D * rinv;
-        const double dvx = I.vx - vj.x, dvy = I.vy - vj.y;
-        s.div = fma(fac, fma(dvx, dx, dvy * dy), s.div);
-        s.rot = fma(fac, fma(dvx, dy, -dvy * dx), s.rot);
+  __device__ static void den_tile(const DI &I, const DenTile &T, DA &s) {
+#pragma unroll 2
+    for (int j = 0; j < kTJ; j += 4) {
+      double dx[4], dy[4], r2[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const double2 xj = T.xy[j + k];
+        dx[k] = I.x - xj.x;
+        dy[k] = I.y - xj.y;
+        if (MINIMG) { dx[k] -= round(dx[k]); dy[k] -= round(dy[k]); }
+        r2[k] = fma(dx[k], dx[k], dy[k] * dy[k]);
       }
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        if (in_support(r2[k], I.hiH2m1)) den_in(I, dx[k], dy[k], r2[k], T.vv[j + k], T.m[j + k], s);
     }
   }
 
   template <bool MINIMG>
-  __device__ static void mw_pair(const DI &I, double2 xj, MW &m) {
-    double dx = I.x - xj.x, dy = I.y - xj.y;
-    if (MINIMG) { dx -= round(dx); dy -= round(dy); }
-    const double r2 = fma(dx, dx, dy * dy);
-    if (r2 < I.H2 && r2 > 0.0) {
-      const double q = r2 * rsqrt_nr(r2) * I.inv_h;
-      m.w += Spline(q).P();
+  __device__ static void mw_tile(const DI &I, const DenTile &T, MW &m) {
+#pragma unroll 4
+    for (int j = 0; j < kTJ; ++j) {
+      double dx = I.x - T.xy[j].x, dy = I.y - T.xy[j].y;
+      if (MINIMG) { dx -= round(dx); dy -= round(dy); }
+      const double r2 = fma(dx, dx, dy * dy);
+      if (in_support(r2, I.hiH2m1)) {
+        Spline sp;
+        sp.template eval<true>(r2 * rsqrt_fast(r2) * I.inv_h);
+        m.w += sp.P;
+      }
     }
   }
 
@@ -136,22 +193,23 @@ struct FastPolicy {
     o[0] = h;
     o[1] = fma(kNorm2d, s.rho, mi * kW0) * inv_h2;
     o[2] = fma(kNorm2d, s.w, kW0);
-    o[3] = -fma(kNorm2d, s.dh, 2.0 * mi * kW0) * inv_h3;
-    o[4] = s.rot * n3;
-    o[5] = -s.div * n3;
+    // reference: rho_dh = (sum -m(2w + q dw) - 2 m_i w0) / h^3, dw = -4 N E
+    o[3] = -fma(kNorm2d, fma(-4.0, s.qe, 2.0 * s.rho), 2.0 * mi * kW0) * inv_h3;
+    o[4] = -4.0 * s.rot * n3;
+    o[5] = 4.0 * s.div * n3;
   }
 
-  struct FI { double x, y, vx, vy, inv_hi, H2, eps2, pri, mb3, ci, K, hi; };
+  struct FI { double x, y, vx, vy, inv_hi, eps2, pri, mb3, ci, hi, K; unsigned hiH2m1; };
   struct FA { double ax, ay, udt, vsig, hdt, hdt0; };
 
-  // force_inv (kernels.cpp:155-172); K = N / h^3 multiplies every SPH term.
+  // force_inv (kernels.cpp:155-172); K = -4 N / h^3 multiplies every SPH pair term.
   __device__ static FI for_i(double2 x, double2 vp, double h, double p, double rho,
                              double rho_dh, double c, double div_v, double rot_v, double) {
     FI I;
     I.x = x.x; I.y = x.y; I.vx = vp.x; I.vy = vp.y;
     I.hi = h;
     I.inv_hi = 1.0 / h;
-    I.H2 = 6.25 * h * h;
+    I.hiH2m1 = (unsigned)hi_word(6.25 * h * h) - 1u;
     I.eps2 = 0.01 * h * h;
     const double irho = 1.0 / rho;
     I.pri = p * irho * irho * fma(0.5 * h * rho_dh, irho, 1.0);
@@ -159,10 +217,12 @@ struct FastPolicy {
     I.ci = c;
     const double bi = adiv / (adiv + fabs(rot_v) + 0.0001 * c * I.inv_hi);
     I.mb3 = -3.0 * bi;
-    I.K = kNorm2d * I.inv_hi * I.inv_hi * I.inv_hi;
+    I.K = -4.0 * kNorm2d * I.inv_hi * I.inv_hi * I.inv_hi;
     return I;
   }
-  __device__ static FA for_zero(double h_dt) { return FA{0.0, 0.0, 0.0, 0.0, 0.0, h_dt}; }
+  // vsig accumulates max_j (c_j - 3 mu b_i) >= 0; -1 marks "no in-support pair" (the
+  // reference then keeps its initial +0.0, kernels.cpp:89)
+  __device__ static FA for_zero(double h_dt) { return FA{0.0, 0.0, 0.0, -1.0, 0.0, h_dt}; }
 
   // tile terms: (m, grav*m, m*p/rho^2, m/rho)
   __device__ static double4 stage_force(double m, double rho, double p, double grav) {
@@ -171,54 +231,86 @@ struct FastPolicy {
     return make_double4(m, grav * m, V * p * irho, V);
   }
 
+  // SPH part of force_pair for one in-support pair; returns the radial factor to add to
+  // the gravity factor (both multiply dx, dy).
+  __device__ __forceinline__ static double for_in(const FI &I, double dx, double dy, double r2,
+                                                  double2 vj, double2 mg, double2 pv, double cj,
+                                                  FA &s) {
+    const double rinv = rsqrt_fast(r2);
+    const double q = r2 * rinv * I.inv_hi;
+    Spline sp;
+    sp.template eval<false>(q);
+    const double g = sp.E * rinv;
+    const double dvx = I.vx - vj.x, dvy = I.vy - vj.y;
+    const double dvdr = fma(dvx, dx, dvy * dy);
+    const double gd = g * dvdr;
+    s.udt = fma(mg.x, gd, s.udt);
+    s.hdt = fma(pv.y, gd, s.hdt);
+    // mu = min(0, dvdr / r): sign test on the high word (ALU), then one DMUL
+    const double mu = (hi_word(dvdr) < 0 ? dvdr : 0.0) * rinv;
+    // vsig = max_j (c_i + c_j - 3 mu b_i) = c_i + max_j (c_j - 3 mu b_i): fl(c_i + x) is
+    // monotonic in x, so adding c_i once at the end gives the same value
+    const double vs = fma(mu, I.mb3, cj);
+    s.vsig = vs > s.vsig ? vs : s.vsig;
+    return fma(mg.x, I.pri, pv.x) * g * I.K;
+  }
+
+  // Four pairs per step: distances and the softened gravity (every active pair,
+  // kernels.cpp:128-131) are straight-line code for the four pairs, so their rsqrt /
+  // Newton chains interleave; the divergent SPH blocks follow in j order. The self pair
+  // has dx = dy = 0 and padding has gm = 0: both contribute exactly zero.
   template <bool MINIMG>
-  __device__ static void for_pair(const FI &I, double2 xj, double2 vj, double2 mg, double2 pv,
-                                  double cj, FA &s) {
-    double dx = I.x - xj.x, dy = I.y - xj.y;
-    if (MINIMG) { dx -= round(dx); dy -= round(dy); }
-    const double r2 = fma(dx, dx, dy * dy);
-    // softened gravity on every active pair (kernels.cpp:128-131); the self pair has
-    // dx = dy = 0 and contributes exactly zero.
-    const double y = rsqrt_nr(r2 + I.eps2);
-    double f = mg.y * (y * y * y);
-    if (r2 < I.H2) {
-      if (r2 > 0.0) {
-        const double rinv = rsqrt_nr(r2);
-        const double q = r2 * rinv * I.inv_hi;
-        const double g = Spline(q).D() * rinv;
-        f = fma(fma(mg.x, I.pri, pv.x) * g, I.K, f);
-        const double dvx = I.vx - vj.x, dvy = I.vy - vj.y;
-        const double dvdr = fma(dvx, dx, dvy * dy);
-        const double gd = g * dvdr;
-        s.udt = fma(mg.x, gd, s.udt);
-        s.hdt = fma(pv.y, gd, s.hdt);
-        const double mu = fmin(0.0, dvdr * rinv);
-        s.vsig = fmax(s.vsig, fma(mu, I.mb3, I.ci + cj));
+  __device__ static void for_tile(const FI &I, const ForTile &T, FA &s) {
+    constexpr int G = SPH_FJ; // pairs whose gravity chains are interleaved
+#pragma unroll 1
+    for (int j = 0; j < kTJ; j += G) {
+      double dx[G], dy[G], r2[G], f[G];
+#pragma unroll
+      for (int k = 0; k < G; ++k) {
+        const double2 xj = T.xy[j + k];
+        dx[k] = I.x - xj.x;
+        dy[k] = I.y - xj.y;
+        if (MINIMG) { dx[k] -= round(dx[k]); dy[k] -= round(dy[k]); }
+        r2[k] = fma(dx[k], dx[k], dy[k] * dy[k]);
+        f[k] = T.mg[j + k].y * rsqrt3_fast(r2[k] + I.eps2);
+      }
+#pragma unroll
+      for (int k = 0; k < G; ++k)
+        if (in_support(r2[k], I.hiH2m1))
+          f[k] += for_in(I, dx[k], dy[k], r2[k], T.vv[j + k], T.mg[j + k], T.pv[j + k], T.c[j + k], s);
+#pragma unroll
+      for (int k = 0; k < G; ++k) {
+        s.ax = fma(-f[k], dx[k], s.ax);
+        s.ay = fma(-f[k], dy[k], s.ay);
       }
     }
-    s.ax = fma(-f, dx, s.ax);
-    s.ay = fma(-f, dy, s.ay);
   }
 
   __device__ static void for_publish(const FI &I, const FA &s, double o[5]) {
     o[0] = s.ax;
     o[1] = s.ay;
     o[2] = I.pri * I.K * s.udt;
-    o[3] = s.vsig;
+    o[3] = s.vsig < 0.0 ? 0.0 : I.ci + s.vsig;
     o[4] = fma(-0.5 * I.hi * I.K, s.hdt, s.hdt0);
   }
 };
 
 void launch_density_fast(const DenArgs &a, int n_items, bool aos, cudaStream_t s) {
   if (n_items <= 0) return;
-  if (aos) density_round_kernel<FastPolicy, true, false><<<n_items, kTI, 0, s>>>(a);
-  else density_round_kernel<FastPolicy, false, false><<<n_items, kTI, 0, s>>>(a);
+  DenArgs b = a;
+  b.n_items = n_items;
+  const int G = pair_grid(n_items), B = kWarpsPerCta * 32;
+  if (aos) density_round_kernel<FastPolicy, true, false><<<G, B, 0, s>>>(b);
+  else density_round_kernel<FastPolicy, false, false><<<G, B, 0, s>>>(b);
 }
 
 void launch_force_fast(const ForArgs &a, int n_items, bool aos, cudaStream_t s) {
   if (n_items <= 0) return;
-  if (aos) force_kernel<FastPolicy, true><<<n_items, kTI, 0, s>>>(a);
-  else force_kernel<FastPolicy, false><<<n_items, kTI, 0, s>>>(a);
+  ForArgs b = a;
+  b.n_items = n_items;
+  const int G = pair_grid(n_items), B = kWarpsPerCta * 32;
+  if (aos) force_kernel<FastPolicy, true><<<G, B, 0, s>>>(b);
+  else force_kernel<FastPolicy, false><<<G, B, 0, s>>>(b);
 }
 
 } // namespace sphb

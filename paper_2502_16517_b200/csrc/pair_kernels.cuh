@@ -2,33 +2,53 @@
 // :535-628), as one CUDA skeleton parameterised by a numerics policy.
 //
 // Work decomposition (replaces the std::thread cell pool, kernels.cpp:492-533):
-//   * one CTA per work item = (cell c, up to kTI local particles of c); one thread per
-//     local particle i, which accumulates its sums in registers over the whole active list
-//     of c in the reference's order (stencil cells in (dy,dx) order, each in local-list
-//     order). There is no reduction across threads and no atomics on the sums, so the
-//     EXACT policy reproduces the reference's summation order bit for bit.
-//   * the active list streams through shared memory in tiles of kTJ particles: every
-//     thread gathers one j record (AoS record or SoA mirror -> SoA tile: the on-the-fly
-//     AoS->SoA conversion), per-j invariants (grav*m, p/rho^2, m/rho) are hoisted into the
-//     tile, and the tile is double-buffered (global loads for tile k+1 are in flight while
-//     tile k is consumed). All lanes of a warp read the same j (shared-memory broadcast).
-//   * the local particles of a cell are assigned to threads in a spatially sorted order
-//     (ilist), so the 32 lanes of a warp are neighbours and take the in-support branch
-//     together; the assignment does not affect any particle's result.
-//   * density's smoothing-length iteration (kernels.cpp:184-192) runs as rounds: particles
-//     that need another round append themselves to a per-cell pending list and the next
-//     launch only processes those (grouped by cell again), instead of re-sweeping tiles.
+//   * one WARP per work item = (cell c, up to 32 local particles of c), one lane per local
+//     particle i. Each lane accumulates its sums in registers over the whole active list of
+//     c in the reference's order (stencil cells in (dy,dx) order, each in local-list
+//     order). No reduction across lanes and no atomics on the sums, so the EXACT policy
+//     reproduces the reference's summation order bit for bit.
+//   * the active list streams through a per-warp shared-memory tile of 32 particles: lane
+//     l gathers active particle (32k + l) — the on-the-fly AoS->SoA conversion, from the
+//     AoS record or the SoA mirror — with the per-j invariants (grav*m, p/rho^2, m/rho)
+//     hoisted into the tile. The next tile's global loads are in flight in registers while
+//     the current tile is consumed; every lane then reads the same j (smem broadcast).
+//     Warps never wait for each other (only __syncwarp), so divergence in one warp does
+//     not stall its neighbours at a CTA barrier.
+//   * the last tile is padded with inert dummies (x = 1e30, m = 0): every policy provably
+//     skips them, so tiles always hold 32 entries and the j loop has a fixed trip count.
+//   * the local particles of a cell are assigned to lanes in a spatially sorted order
+//     (ilist: 8x8 sub-cell Morton bins), so the 32 lanes of a warp are neighbours and take
+//     the in-support branch together; the assignment does not affect any result.
+//   * density's smoothing-length iteration (kernels.cpp:184-192) runs as rounds: lanes that
+//     need another round append their particle to a per-cell pending list and the next
+//     launch processes only those, regrouped into full warps by cell.
 #pragma once
 #include "sph_common.cuh"
 
 namespace sphb {
 
-constexpr int kTI = 128; // local particles (threads) per CTA
-constexpr int kTJ = 128; // active particles per shared-memory tile
+constexpr int kTI = 32;        // local particles per work item (one warp)
+constexpr int kTJ = 32;        // active particles per shared-memory tile
+constexpr int kWarpsPerCta = 4;
+constexpr double kDummyX = 1.0e30;
+#ifndef SPH_SPLINE3
+#define SPH_SPLINE3 0
+#endif
+#ifndef SPH_FJ
+#define SPH_FJ 2 // force: pairs per interleaved gravity group
+#endif
+// min resident CTAs per SM requested from ptxas (caps registers: 65536 / (128 * MINB))
+#ifndef SPH_MINB_DEN
+#define SPH_MINB_DEN 5
+#endif
+#ifndef SPH_MINB_FOR
+#define SPH_MINB_FOR 5
+#endif
 
 struct DenArgs {
   Geom g;
   const Item *items;
+  int n_items;
   const int *list;      // slots, indexed by Item::start
   int round;            // h-iteration round (0..29)
   double target, h_max;
@@ -44,6 +64,7 @@ struct DenArgs {
 struct ForArgs {
   Geom g;
   const Item *items;
+  int n_items;
   const int *list;
   double grav;
   const Particle *aos;
@@ -81,7 +102,7 @@ template <> struct JSrc<false> {
   __device__ __forceinline__ double h_dt(int s) const { return f.h_dt[s]; }
 };
 
-// Per-CTA active-list layout: stencil cells, their slot ranges and prefix offsets.
+// Per-warp active-list layout: stencil cells, their slot ranges and prefix offsets.
 struct ActiveLayout {
   int n;          // stencil cells
   int na;         // active particles
@@ -126,25 +147,31 @@ struct ForTile {
   double c[kTJ];
 };
 
+__device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
+__device__ __forceinline__ int warp_in_cta() { return threadIdx.x >> 5; }
+
 // ---------------------------------------------------------------------------------------
 // Density round (also the mean_wcount pass of make_particles when MEANW).
 // ---------------------------------------------------------------------------------------
 template <class P, bool AOS, bool MEANW>
-__global__ void __launch_bounds__(kTI) density_round_kernel(DenArgs A) {
-  __shared__ DenTile tile[2];
-  __shared__ ActiveLayout L;
-  const Item it = A.items[blockIdx.x];
-  const int t = threadIdx.x;
-  if (t == 0) build_active(A.g, it.cell, L);
+__global__ void __launch_bounds__(kWarpsPerCta * 32, SPH_MINB_DEN) density_round_kernel(DenArgs A) {
+  __shared__ DenTile tiles[kWarpsPerCta];
+  __shared__ ActiveLayout lay[kWarpsPerCta];
+  const int w = warp_in_cta(), lane = lane_id();
+  const int item_idx = blockIdx.x * kWarpsPerCta + w;
+  if (item_idx >= A.n_items) return; // whole warp
+  DenTile &T = tiles[w];
+  ActiveLayout &L = lay[w];
+  const Item it = A.items[item_idx];
+  if (lane == 0) build_active(A.g, it.cell, L);
   JSrc<AOS> src;
   if constexpr (AOS) src.p = A.aos; else src.f = A.soa;
-  const bool live = t < it.count;
-  const bool warp_live = (t & ~31) < it.count;
-  const int slot = A.list[it.start + (live ? t : 0)];
+  const bool live = lane < it.count;
+  const int slot = A.list[it.start + (live ? lane : 0)];
   const double2 xi = src.x(slot), vi = src.vp(slot);
   const double mi = src.m(slot);
-  double h = (A.round == 0) ? src.h(slot) : A.hcur[slot];
-  __syncthreads();
+  const double h = (A.round == 0) ? src.h(slot) : A.hcur[slot];
+  __syncwarp();
   const bool minimg = P::kExactOrder || !A.g.use_shift;
   const int na = L.na, ntiles = (na + kTJ - 1) / kTJ;
 
@@ -152,53 +179,38 @@ __global__ void __launch_bounds__(kTI) density_round_kernel(DenArgs A) {
   typename P::DA s = P::den_zero();
   typename P::MW mw = P::mw_zero();
 
-  // prologue: gather tile 0
-  double2 rx = make_double2(0.0, 0.0), rv = rx;
-  double rm = 0.0;
+  double2 rx, rv;
+  double rm;
   auto gather = [&](int k) {
-    int p = k * kTJ + t;
+    const int p = k * kTJ + lane;
     if (p < na) {
       int nb;
-      int sj = active_slot(L, p, nb);
+      const int sj = active_slot(L, p, nb);
       rx = src.x(sj);
       rv = src.vp(sj);
       rm = src.m(sj);
       if (!minimg) { rx.x += L.sx[nb]; rx.y += L.sy[nb]; }
+    } else { // inert padding (skipped by every policy)
+      rx = make_double2(kDummyX, kDummyX);
+      rv = make_double2(0.0, 0.0);
+      rm = 0.0;
     }
   };
-  auto store = [&](DenTile &T) {
-    T.xy[t] = rx;
-    T.vv[t] = rv;
-    T.m[t] = rm;
-  };
-  if (ntiles > 0) {
-    gather(0);
-    store(tile[0]);
-  }
-  __syncthreads();
+  if (ntiles > 0) gather(0);
   for (int k = 0; k < ntiles; ++k) {
-    if (k + 1 < ntiles) gather(k + 1);
-    const DenTile &T = tile[k & 1];
-    const int tn = min(kTJ, na - k * kTJ);
-    if (warp_live) {
-      if (MEANW) {
-        if (minimg) {
-#pragma unroll 4
-          for (int j = 0; j < tn; ++j) P::template mw_pair<true>(I, T.xy[j], mw);
-        } else {
-#pragma unroll 4
-          for (int j = 0; j < tn; ++j) P::template mw_pair<false>(I, T.xy[j], mw);
-        }
-      } else if (minimg) {
-#pragma unroll 4
-        for (int j = 0; j < tn; ++j) P::template den_pair<true>(I, T.xy[j], T.vv[j], T.m[j], s);
-      } else {
-#pragma unroll 4
-        for (int j = 0; j < tn; ++j) P::template den_pair<false>(I, T.xy[j], T.vv[j], T.m[j], s);
-      }
+    T.xy[lane] = rx;
+    T.vv[lane] = rv;
+    T.m[lane] = rm;
+    __syncwarp();
+    if (k + 1 < ntiles) gather(k + 1); // loads in flight during the tile
+    if (MEANW) {
+      if (minimg) P::template mw_tile<true>(I, T, mw);
+      else P::template mw_tile<false>(I, T, mw);
+    } else {
+      if (minimg) P::template den_tile<true>(I, T, s);
+      else P::template den_tile<false>(I, T, s);
     }
-    if (k + 1 < ntiles) store(tile[(k + 1) & 1]);
-    __syncthreads();
+    __syncwarp();
   }
   if (!live) return;
   if (MEANW) {
@@ -231,32 +243,35 @@ __global__ void __launch_bounds__(kTI) density_round_kernel(DenArgs A) {
 // Force sweep.
 // ---------------------------------------------------------------------------------------
 template <class P, bool AOS>
-__global__ void __launch_bounds__(kTI) force_kernel(ForArgs A) {
-  __shared__ ForTile tile[2];
-  __shared__ ActiveLayout L;
-  const Item it = A.items[blockIdx.x];
-  const int t = threadIdx.x;
-  if (t == 0) build_active(A.g, it.cell, L);
+__global__ void __launch_bounds__(kWarpsPerCta * 32, SPH_MINB_FOR) force_kernel(ForArgs A) {
+  __shared__ ForTile tiles[kWarpsPerCta];
+  __shared__ ActiveLayout lay[kWarpsPerCta];
+  const int w = warp_in_cta(), lane = lane_id();
+  const int item_idx = blockIdx.x * kWarpsPerCta + w;
+  if (item_idx >= A.n_items) return;
+  ForTile &T = tiles[w];
+  ActiveLayout &L = lay[w];
+  const Item it = A.items[item_idx];
+  if (lane == 0) build_active(A.g, it.cell, L);
   JSrc<AOS> src;
   if constexpr (AOS) src.p = A.aos; else src.f = A.soa;
-  const bool live = t < it.count;
-  const bool warp_live = (t & ~31) < it.count;
-  const int slot = A.list[it.start + (live ? t : 0)];
+  const bool live = lane < it.count;
+  const int slot = A.list[it.start + (live ? lane : 0)];
   typename P::FI I = P::for_i(src.x(slot), src.vp(slot), src.h(slot), src.pr(slot),
                               src.rho(slot), src.rho_dh(slot), src.c(slot), src.div_v(slot),
                               src.rot_v(slot), A.grav);
   typename P::FA s = P::for_zero(src.h_dt(slot));
-  __syncthreads();
+  __syncwarp();
   const bool minimg = P::kExactOrder || !A.g.use_shift;
   const int na = L.na, ntiles = (na + kTJ - 1) / kTJ;
 
-  double2 rx = make_double2(0.0, 0.0), rv = rx;
-  double rm = 0.0, rrho = 1.0, rp = 0.0, rc = 0.0;
+  double2 rx, rv;
+  double rm, rrho, rp, rc;
   auto gather = [&](int k) {
-    int p = k * kTJ + t;
+    const int p = k * kTJ + lane;
     if (p < na) {
       int nb;
-      int sj = active_slot(L, p, nb);
+      const int sj = active_slot(L, p, nb);
       rx = src.x(sj);
       rv = src.vp(sj);
       rm = src.m(sj);
@@ -264,38 +279,25 @@ __global__ void __launch_bounds__(kTI) force_kernel(ForArgs A) {
       rp = src.pr(sj);
       rc = src.c(sj);
       if (!minimg) { rx.x += L.sx[nb]; rx.y += L.sy[nb]; }
+    } else { // inert padding: r2 <= 0 (exact) or gm = 0 (fast)
+      rx = make_double2(kDummyX, kDummyX);
+      rv = make_double2(0.0, 0.0);
+      rm = 0.0; rrho = 1.0; rp = 0.0; rc = 0.0;
     }
   };
-  auto store = [&](ForTile &T) {
-    T.xy[t] = rx;
-    T.vv[t] = rv;
-    double4 d = P::stage_force(rm, rrho, rp, A.grav); // (m, gm, pv.x, pv.y)
-    T.mg[t] = make_double2(d.x, d.y);
-    T.pv[t] = make_double2(d.z, d.w);
-    T.c[t] = rc;
-  };
-  if (ntiles > 0) {
-    gather(0);
-    store(tile[0]);
-  }
-  __syncthreads();
+  if (ntiles > 0) gather(0);
   for (int k = 0; k < ntiles; ++k) {
+    T.xy[lane] = rx;
+    T.vv[lane] = rv;
+    const double4 d = P::stage_force(rm, rrho, rp, A.grav); // (m, gm, pv.x, pv.y)
+    T.mg[lane] = make_double2(d.x, d.y);
+    T.pv[lane] = make_double2(d.z, d.w);
+    T.c[lane] = rc;
+    __syncwarp();
     if (k + 1 < ntiles) gather(k + 1);
-    const ForTile &T = tile[k & 1];
-    const int tn = min(kTJ, na - k * kTJ);
-    if (warp_live) {
-      if (minimg) {
-#pragma unroll 2
-        for (int j = 0; j < tn; ++j)
-          P::template for_pair<true>(I, T.xy[j], T.vv[j], T.mg[j], T.pv[j], T.c[j], s);
-      } else {
-#pragma unroll 2
-        for (int j = 0; j < tn; ++j)
-          P::template for_pair<false>(I, T.xy[j], T.vv[j], T.mg[j], T.pv[j], T.c[j], s);
-      }
-    }
-    if (k + 1 < ntiles) store(tile[(k + 1) & 1]);
-    __syncthreads();
+    if (minimg) P::template for_tile<true>(I, T, s);
+    else P::template for_tile<false>(I, T, s);
+    __syncwarp();
   }
   if (!live) return;
   double o[5]; // a0, a1, u_dt, v_sig, h_dt
@@ -309,10 +311,6 @@ __global__ void __launch_bounds__(kTI) force_kernel(ForArgs A) {
   }
 }
 
-// Host-side launchers (defined in kernels_exact.cu / kernels_fast.cu).
-void launch_density_exact(const DenArgs &a, int n_items, bool aos, bool meanw, cudaStream_t s);
-void launch_force_exact(const ForArgs &a, int n_items, bool aos, cudaStream_t s);
-void launch_density_fast(const DenArgs &a, int n_items, bool aos, cudaStream_t s);
-void launch_force_fast(const ForArgs &a, int n_items, bool aos, cudaStream_t s);
+inline int pair_grid(int n_items) { return (n_items + kWarpsPerCta - 1) / kWarpsPerCta; }
 
 } // namespace sphb
