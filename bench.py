@@ -1,16 +1,27 @@
 """bench.py — full SPH step (kick1 -> drift -> rebin -> density -> force -> kick2) on B200.
 
-Workload (BASELINE.json configs[1]): uniform 2-D box, n = 2^21 particles, ppc = 1024,
-seed 42, the reference's own initial condition (grid.cpp:76-143) generated on the device
-with EXACT numerics (byte-identical to the reference IC); synthetic data, no checkpoints.
+Workload (BASELINE.json configs[1]): uniform 2-D periodic box, n = 2^21 particles,
+ppc = 1024 (nx = 45, 2025 cells), seed 42 — the reference's own initial condition
+(make_particles, grid.cpp:76-143), generated on the device with EXACT numerics
+(byte-identical to the reference IC, tests/test_gpu_parity.py). Synthetic data.
 
-Headline metric: particle-pair interactions/s over density + force (sum over cells of
-nl*na*rounds for density plus nl*na for force, per step, divided by the step time), with
-SPH steps/s reported beside it. See DESIGN.md §6 for the roofline definitions.
+Metric: particle-pair interactions/s over density + force. The pair count of the workload
+is implementation-independent: sum over cells of nl*na for density plus the same for
+force (one pass each, kernels.cpp:204-303), per step, divided by the step time; extra
+h-iteration rounds (kernels.cpp:184-192) are work the step has to do, not extra credit.
+SPH steps/s is reported beside it.
+
+  value  : device-resident step (state stays in HBM), CUDA events on the library stream
+  e2e    : the same step through the C-ABI on HOST records (sph_step_host): every step
+           copies all records host->device and device->host (pinned host memory)
+  roofline: force kernel (largest share of the step) vs the FP64 pipe peak measured
+           live by a DFMA microbenchmark (sph_fp64_peak); HBM kernels beside it
+  cpu_baseline: the unmodified reference (oracle/_ref) on this host's cores, one step on
+           a bounded sample of cells scaled by pair count (oracle/ref_bench.py)
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-Multi-GPU (torchrun, N>1): weak scaling of independent replicas (one box per rank);
-rank 0 prints the JSON line with the max-over-ranks time.
+N>1 (torchrun): weak scaling, one independent full-size replica per GPU (the pair
+sweeps have no cross-replica exchange); time = max over ranks.
 """
 from __future__ import annotations
 
@@ -30,13 +41,19 @@ sys.path.insert(0, ROOT)
 
 METRIC = "particle-pair interactions/sec (density+force)"
 UNIT = "pairs/s"
-
-# algorithmic flops per pair: density 13 + 38 f_in + 11 f_<1.5 + 11 f_<0.5,
-# force 22 + 45 f_in + 5 f_<1.5 + 5 f_<0.5 (counted from the reference source, kernels.cpp:97-153)
+F_IN_REF = (0.2236, 0.0804, 0.0089)  # SURVEY.md §8(d), reference IC at ppc 1024
 
 
 def flops_per_pair(f_in, f15, f05):
+    """Algorithmic flops per evaluated pair counted from the reference source
+    (SURVEY.md §8(d)): density 13 + 38 f_in + 11 f_<1.5 + 11 f_<0.5,
+    force 22 + 45 f_in + 5 f_<1.5 + 5 f_<0.5."""
     return 13 + 38 * f_in + 11 * f15 + 11 * f05, 22 + 45 * f_in + 5 * f15 + 5 * f05
+
+
+# algorithmic bytes per particle of the streaming kernels (descriptor bytes in + out,
+# kernels.cpp:808-859): drift 52+28, kick1 48+32, kick2 112+80
+LINEAR_BYTES = {"kick1": 80, "drift": 80, "kick2": 192}
 
 
 def load_peaks():
@@ -45,6 +62,18 @@ def load_peaks():
         with open(p) as f:
             return json.load(f), "measured"
     return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0}, "fallback"
+
+
+def load_traffic():
+    """dram bytes per launch of the force kernel from the committed ncu capture."""
+    p = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        k = d["kernels"]["force_kernel<FastPolicy>"]
+        return k["dram_bytes_read"] + k["dram_bytes_write"], d.get("source", p)
+    except Exception:
+        return None, None
 
 
 class ClockSampler:
@@ -79,27 +108,27 @@ class ClockSampler:
 
     def summary(self):
         if not self.samples:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
         sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
         mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         reasons = sorted({names[i] for s in self.samples for i in range(4)
                           if len(s) > i + 2 and s[i + 2].lower() == "active"})
         return {"sm_mhz": statistics.median(sm) if sm else None,
-                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons}
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.samples)}
 
 
-def dist_init(args):
+def dist_init():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
     if world > 1:
         import torch
         import torch.distributed as dist
-        local = int(os.environ.get("LOCAL_RANK", "0"))
         torch.cuda.set_device(local)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-        return rank, world, local
-    return 0, 1, 0
+    return rank, world, local
 
 
 def barrier(world):
@@ -118,92 +147,200 @@ def allmax(v, world):
     return float(t.item())
 
 
+def pair_fractions(store, grid, ncells_sample=64, seed=1):
+    """In-support fractions of the current state on a sample of cells (oracle stats)."""
+    from oracle import Oracle
+    orc = Oracle()
+    rng = np.random.default_rng(seed)
+    mask = np.zeros(grid.cells(), np.uint8)
+    mask[rng.choice(grid.cells(), size=min(ncells_sample, grid.cells()), replace=False)] = 1
+    st = orc.pair_stats(store.recs, grid.nx, grid.ny, grid.cell_begin, grid.local_idx,
+                        cell_mask=mask)
+    return st[2] / st[0], st[3] / st[0], st[4] / st[0]
+
+
+def config_block(args, grid, world):
+    return {"workload": f"full SPH step, uniform 2-D box, n={args.n}, ppc={args.ppc}",
+            "n": args.n, "ppc": args.ppc, "nx": grid.nx if grid else None, "seed": args.seed,
+            "dt": args.dt, "numerics": args.numerics, "layout": args.layout,
+            "l2": "inputs larger than L2 (AoS mirror 0.57 GB + SoA mirror 0.44 GB at n=2^21)",
+            "parallelism": f"replicas x{world}" if world > 1 else "single GPU"}
+
+
 def run_ours(args, rank, world, local):
     import paper_2502_16517_b200 as pkg
     from paper_2502_16517_b200 import DeviceLayout, Numerics
 
-    n, ppc, seed = args.n, args.ppc, args.seed
     ctx = pkg.Context(local, numerics=Numerics[args.numerics.capitalize()],
                       layout=DeviceLayout[args.layout.capitalize()])
     t0 = time.time()
-    store, grid, par = ctx.make_particles(n, ppc, seed)
+    store, grid, par = ctx.make_particles(args.n, args.ppc, args.seed)
     t_ic = time.time() - t0
     par.dt = args.dt
+    workload_pairs = 2 * ctx.stats()["active_pairs"]
 
-    # pair statistics for the flop count (one density round at the IC's h)
-    fpp = None
-    if rank == 0 and args.count_flops:
-        from oracle import Oracle
-        orc = Oracle()
-        # sampled cells: the in-support fractions are cell-local statistics
-        cs = orc.pair_stats(store.recs, grid.nx, grid.ny, grid.cell_begin, grid.local_idx, 0) \
-            if n <= 300000 else None
-        if cs is not None:
-            fin, f15, f05 = cs[2] / cs[0], cs[3] / cs[0], cs[4] / cs[0]
-        else:
-            fin, f15, f05 = 0.2236, 0.0804, 0.0089  # SURVEY.md §8(d), reference IC, ppc 1024
-        fpp = flops_per_pair(fin, f15, f05) + (fin, f15, f05)
-
+    # ---- device-resident timed region ----
     for _ in range(args.warmup):
         ctx.step(par)
-    barrier(world)
     ctx.synchronize()
+    barrier(world)
     launches0 = ctx.launch_count()
     phase = np.zeros(6)
-    den_pairs = for_pairs = 0
+    den_eval = 0
+    steps_ms = []
     with ClockSampler(local) as clk:
-        tstep = []
         for _ in range(args.steps):
             ms = ctx.step(par)
-            st = ctx.stats()
-            den_pairs += st["density_pairs"]
-            for_pairs += st["force_pairs"]
+            den_eval += ctx.stats()["density_pairs"]
             phase += ms
-            tstep.append(float(ms.sum()))
+            steps_ms.append(float(ms.sum()))
     ctx.synchronize()
     launches = ctx.launch_count() - launches0
     barrier(world)
-    total_ms = allmax(float(np.sum(tstep)), world)
+    total_ms = allmax(float(np.sum(steps_ms)), world)
     ms_per_step = total_ms / args.steps
-    pairs_per_step = (den_pairs + for_pairs) / args.steps
-    value = pairs_per_step * world / (ms_per_step * 1e-3)
+    value = workload_pairs * world / (ms_per_step * 1e-3)
+    ph = phase / args.steps
+    names = ["kick1", "drift", "rebin", "density", "force", "kick2"]
+
     out = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic (reference make_particles IC, uniform 2-D, seed 42)",
-        "config": {"workload": f"full SPH step, uniform box, n={n}, ppc={ppc}",
-                   "n": n, "ppc": ppc, "nx": grid.nx, "numerics": args.numerics,
-                   "layout": args.layout, "dt": par.dt,
-                   "l2": "inputs larger than L2 (AoS mirror 0.57 GB + SoA mirror)",
-                   "parallelism": f"replicas x{world}"},
+        "data": "synthetic: reference make_particles IC (uniform random 2-D, seed 42), "
+                "generated on device, byte-identical to the reference",
+        "config": config_block(args, grid, world),
         "steps_per_s": 1e3 / ms_per_step * world,
-        "phase_ms": dict(zip(["kick1", "drift", "rebin", "density", "force", "kick2"],
-                             (phase / args.steps).round(4).tolist())),
-        "density_pairs_per_step": den_pairs / args.steps,
-        "force_pairs_per_step": for_pairs / args.steps,
+        "workload_pairs_per_step": workload_pairs,
+        "density_pairs_evaluated_per_step": den_eval / args.steps,
+        "phase_ms": dict(zip(names, ph.round(4).tolist())),
         "ic_seconds": round(t_ic, 2),
         "gpu_launches": launches,
+        "gpu_launches_per_step": launches / args.steps,
         "clocks": clk.summary(),
     }
+
+    # ---- e2e: the same step through the C-ABI on pinned host records ----
+    e2e_steps = max(1, args.e2e_steps)
+    ctx.host_register(store.recs)
+    try:
+        ctx.step_host(par)  # warm-up
+        barrier(world)
+        wall = []
+        dev = np.zeros(8)
+        for _ in range(e2e_steps):
+            t0 = time.perf_counter()
+            dev += ctx.step_host(par)
+            wall.append(time.perf_counter() - t0)
+        barrier(world)
+    finally:
+        ctx.host_unregister(store.recs)
+    e2e_s = allmax(float(np.mean(wall)), world)
+    nbytes = store.recs.nbytes
+    out["e2e"] = {"value": workload_pairs * world / e2e_s, "unit": UNIT,
+                  "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": nbytes,
+                  "ms_per_step": e2e_s * 1e3, "steps": e2e_steps,
+                  "api": "sph_step_host (C-ABI, host Particle records in and out)",
+                  "device_ms": dict(zip(["h2d"] + names + ["d2h"],
+                                        (dev / e2e_steps).round(3).tolist()))}
+
     if rank == 0:
         fp64 = ctx.fp64_peak_tflops()
-        out["fp64_peak_tflops_measured"] = fp64
-        if fpp:
-            dfl, ffl, fin, f15, f05 = fpp
-            dms = phase[3] / args.steps
-            fms = phase[4] / args.steps
-            ach_f = ffl * (for_pairs / args.steps) / (fms * 1e-3) / 1e12
-            out["roofline"] = {"bound": "fp64", "kernel": "force_kernel<FastPolicy>",
-                               "achieved": ach_f, "peak": fp64, "unit": "TFLOP/s",
-                               "frac": ach_f / fp64, "traffic": None,
-                               "flops_per_pair": ffl,
-                               "peak_source": "DFMA microbenchmark in this run (sph_fp64_peak)"}
-            out["roofline_density"] = {"achieved": dfl * (den_pairs / args.steps) / (dms * 1e-3) / 1e12,
-                                       "flops_per_pair": dfl}
-            out["pair_fractions"] = {"f_in": fin, "f_lt_1.5": f15, "f_lt_0.5": f05}
+        peaks, src = load_peaks()
+        try:
+            fin, f15, f05 = pair_fractions(_host_state(ctx, store), grid)
+        except Exception:
+            fin, f15, f05 = F_IN_REF
+        dfl, ffl = flops_per_pair(fin, f15, f05)
+        fpairs = workload_pairs / 2
+        ach_f = ffl * fpairs / (ph[4] * 1e-3) / 1e12
+        ach_d = dfl * (den_eval / args.steps) / (ph[3] * 1e-3) / 1e12
+        traffic, tsrc = load_traffic()
+        out["roofline"] = {
+            "bound": "fp64", "kernel": "force_kernel<FastPolicy>", "achieved": ach_f,
+            "peak": fp64, "unit": "TFLOP/s", "frac": ach_f / fp64, "traffic": traffic,
+            "traffic_source": tsrc,
+            "flops_per_pair": ffl, "pairs_per_launch": fpairs, "launch_ms": ph[4],
+            "peak_source": "FP64 DFMA microbenchmark run in this process (sph_fp64_peak); "
+                           "nominal 37.2 TFLOP/s at 1965 MHz",
+        }
+        out["roofline_density"] = {"achieved": ach_d, "frac": ach_d / fp64,
+                                   "flops_per_pair": dfl, "unit": "TFLOP/s"}
+        hbm = peaks.get("hbm_gbs", 6650.0)
+        out["roofline_linear"] = {
+            k: {"achieved_gbs": LINEAR_BYTES[k] * args.n / (ph[names.index(k)] * 1e-3) / 1e9,
+                "peak_gbs": hbm, "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({src})",
+                "frac": LINEAR_BYTES[k] * args.n / (ph[names.index(k)] * 1e-3) / 1e9 / hbm}
+            for k in LINEAR_BYTES}
+        out["pair_fractions"] = {"f_in": fin, "f_lt_1.5": f15, "f_lt_0.5": f05}
+        if world == 1 and args.cpu_baseline:
+            out["cpu_baseline"] = cpu_baseline(ctx, store, grid, par, args)
     ctx.close()
     return out
+
+
+def _host_state(ctx, store):
+    """Current device state as host records (for statistics and the CPU baseline)."""
+    import paper_2502_16517_b200 as pkg
+    recs = ctx.read_records()
+    return pkg.ParticleStore(recs, np.arange(len(recs), dtype=np.int64), pkg.Layout.Continuous)
+
+
+def cpu_baseline(ctx, store, grid, par, args):
+    from oracle.ref_bench import ReferenceStepper
+    st = _host_state(ctx, store)
+    stepper = ReferenceStepper(st.recs, args.ppc, par.as_array(), sample_pairs=args.cpu_sample_pairs)
+    t = stepper.step()
+    return {"value": t["workload_pairs"] / t["step"], "unit": UNIT,
+            "cores": stepper.threads, "kind": "reference",
+            "step_seconds": t["step"], "measured_seconds": t["measured_seconds"],
+            "sample": f"one reference step (kick1, drift, build_grid, kick2 on all {args.n} "
+                      f"particles; density and force on {100 * t['sample_fraction']:.1f}% of the "
+                      f"pair work, random cells, scaled by pair count) of the same workload "
+                      f"state; oracle/_ref built from /root/reference; wall clock",
+            "phase_seconds": {k: round(t[k], 4) for k in
+                              ("kick1", "drift", "rebin", "density", "force", "kick2")}}
+
+
+def run_reference(args, rank, world, local):
+    """The reference's own CPU implementation (oracle/_ref) on this host's cores."""
+    if rank != 0:
+        return None
+    import paper_2502_16517_b200 as pkg
+    from oracle import ref_available
+    from oracle.ref_bench import ReferenceStepper
+    if not ref_available():
+        return {"impl": "reference", "unavailable": "oracle/_ref was not built (needs /root/reference)"}
+    # IC: identical bytes to reference make_particles (which needs ~4 min on 8 cores at
+    # 2^21); produced by the device IC path, outside the timed region.
+    with pkg.Context(local) as ctx:
+        store, grid, par = ctx.make_particles(args.n, args.ppc, args.seed)
+    par.dt = args.dt
+    stepper = ReferenceStepper(store.recs, args.ppc, par.as_array(),
+                               sample_pairs=args.ref_sample_pairs)
+    for _ in range(args.warmup):
+        stepper.step()
+    ts = [stepper.step() for _ in range(args.steps)]
+    step_s = float(np.mean([t["step"] for t in ts]))
+    pairs = ts[0]["workload_pairs"]
+    v = pairs / step_s
+    return {
+        "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_s * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic: reference make_particles IC (uniform random 2-D, seed 42)",
+        "config": config_block(args, grid, 1),
+        "steps_per_s": 1.0 / step_s,
+        "workload_pairs_per_step": pairs,
+        "phase_seconds": {k: round(float(np.mean([t[k] for t in ts])), 4)
+                          for k in ("kick1", "drift", "rebin", "density", "force", "kick2")},
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": stepper.threads, "kind": "reference",
+                         "sample": f"each step: linear kernels + build_grid on all particles, "
+                                   f"density/force on {100 * ts[0]['sample_fraction']:.1f}% of "
+                                   f"the pair work (random cells), scaled by pair count"},
+        "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "gpu_launches": 0,
+    }
 
 
 def main():
@@ -218,14 +355,17 @@ def main():
     ap.add_argument("--dt", type=float, default=1e-4)
     ap.add_argument("--numerics", default="fast", choices=["fast", "exact"])
     ap.add_argument("--layout", default="resident", choices=["resident", "aos", "convert"])
-    ap.add_argument("--count-flops", type=int, default=1)
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--cpu-baseline", type=int, default=1)
+    ap.add_argument("--cpu-sample-pairs", type=float, default=8e8)
+    ap.add_argument("--ref-sample-pairs", type=float, default=1.2e9)
     args = ap.parse_args()
-    rank, world, local = dist_init(args)
+    rank, world, local = dist_init()
     if args.impl == "reference":
-        print(json.dumps({"impl": "reference", "unavailable": "not implemented yet"}))
-        return
-    out = run_ours(args, rank, world, local)
-    if rank == 0:
+        out = run_reference(args, rank, world, local)
+    else:
+        out = run_ours(args, rank, world, local)
+    if rank == 0 and out is not None:
         print(json.dumps(out))
 
 

@@ -120,6 +120,16 @@ int sph_sweep(sph_ctx *ctx, int kernel, const sph_params *par, int path, int ord
 int sph_run_sweep(sph_ctx *ctx, int kernel, void *const *recs, const sph_params *par,
                   int path, int order, int guard, sph_times *times);
 
+/* One leapfrog step on HOST records (the end-to-end drop-in): every record of the bound
+ * order is copied host->device, the step runs on the device (kick1 -> drift -> rebin ->
+ * density -> force -> kick2), and every record is copied back. recs in the bound order.
+ * kernel_ms (optional, 8 entries): H2D, the six phases, D2H (device time). */
+int sph_step_host(sph_ctx *ctx, void *const *recs, const sph_params *par, double *kernel_ms);
+
+/* Page-lock a host range for full-bandwidth copies (cudaHostRegister); optional. */
+int sph_host_register(sph_ctx *ctx, void *base, uint64_t bytes);
+int sph_host_unregister(sph_ctx *ctx, void *base);
+
 /* Rebuild the cell lists on the device after particles moved (build_grid,
  * grid.cpp:145-184): cell = clamp(floor(x*nx)), list order by ParticleStore::all rank. */
 int sph_rebin(sph_ctx *ctx);

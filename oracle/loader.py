@@ -68,7 +68,8 @@ class Oracle:
         lib.orc_make_proto.argtypes = [C.c_int64, C.c_int, C.c_uint64, _recp]
         lib.orc_make_particles.restype = C.c_int
         lib.orc_make_particles.argtypes = [C.c_int64, C.c_int, C.c_uint64, _recp, _f64p, C.c_int]
-        lib.orc_pair_stats.argtypes = [_recp, C.c_int, C.c_int, _i64p, _i64p, C.c_int, _i64p]
+        lib.orc_pair_stats.argtypes = [_recp, C.c_int, C.c_int, _i64p, _i64p, C.c_void_p, C.c_int,
+                                       _i64p]
         for name in ("orc_drift_one", "orc_kick1_one", "orc_kick2_one"):
             getattr(lib, name).argtypes = [C.c_void_p, _f64p]
         self.lib = lib
@@ -111,9 +112,12 @@ class Oracle:
         self.lib.orc_make_particles(n, ppc, seed, out, par, threads or self.threads)
         return out, SphParams.from_array(par)
 
-    def pair_stats(self, recs, nx, ny, cb, li, threads=None) -> np.ndarray:
+    def pair_stats(self, recs, nx, ny, cb, li, threads=None, cell_mask=None) -> np.ndarray:
+        """[active pairs, r2>0, q<2.5, q<1.5, q<0.5] over the (masked) cells."""
         out = np.zeros(5, np.int64)
-        self.lib.orc_pair_stats(recs, nx, ny, cb, li, threads or self.threads, out)
+        m = None if cell_mask is None else np.ascontiguousarray(cell_mask, np.uint8)
+        self.lib.orc_pair_stats(recs, nx, ny, cb, li, None if m is None else m.ctypes.data,
+                                threads or self.threads, out)
         return out
 
     def one(self, which: str, rec: np.ndarray, par) -> None:

@@ -503,9 +503,11 @@ int orc_make_particles(int64_t n, int ppc, uint64_t seed, orc_particle *out, dou
 }
 
 /* Pair statistics of one density round at the records' current h:
- * counts of active pairs, pairs with r2 > 0, and pairs with q < 2.5 / 1.5 / 0.5. */
+ * counts of active pairs, pairs with r2 > 0, and pairs with q < 2.5 / 1.5 / 0.5, over the
+ * cells with cell_mask[c] != 0 (all cells when cell_mask is NULL). */
 void orc_pair_stats(orc_particle *recs, int nx, int ny, const int64_t *cell_begin,
-                    const int64_t *local_idx, int threads, int64_t *out5) {
+                    const int64_t *local_idx, const uint8_t *cell_mask, int threads,
+                    int64_t *out5) {
   grid_t g = {recs, nx, ny, 0.0, cell_begin, local_idx};
   int nc = nx * ny;
   int64_t cap = max_active(&g);
@@ -516,6 +518,7 @@ void orc_pair_stats(orc_particle *recs, int nx, int ny, const int64_t *cell_begi
     int64_t *act = (int64_t *)malloc(sizeof(int64_t) * (size_t)(cap > 0 ? cap : 1));
 #pragma omp for schedule(dynamic, 1)
     for (int c = 0; c < nc; ++c) {
+      if (cell_mask && !cell_mask[c]) continue;
       int64_t na = active_of(&g, c, act);
       for (int64_t t = cell_begin[c]; t < cell_begin[c + 1]; ++t) {
         const orc_particle *pi = &recs[local_idx[t]];

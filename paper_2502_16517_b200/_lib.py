@@ -53,6 +53,9 @@ SIGNATURES = {
                                 C.c_int, C.POINTER(SphTimesC)]),
     "sph_rebin": (C.c_int, [_vp]),
     "sph_step": (C.c_int, [_vp, C.POINTER(SphParamsC), _vp]),
+    "sph_step_host": (C.c_int, [_vp, _vp, C.POINTER(SphParamsC), _vp]),
+    "sph_host_register": (C.c_int, [_vp, _vp, C.c_uint64]),
+    "sph_host_unregister": (C.c_int, [_vp, _vp]),
     "sph_make_particles": (C.c_int, [_vp, C.c_int64, C.c_int, C.c_uint64, C.POINTER(SphParamsC)]),
     "sph_read_records": (C.c_int, [_vp, _vp]),
     "sph_get_stats": (C.c_int, [_vp, C.POINTER(SphStatsC)]),

@@ -216,7 +216,7 @@ struct sph_ctx {
 
   sph_stats stats{};
   int64_t launches = 0;
-  cudaEvent_t ev[16]{};
+  cudaEvent_t ev[20]{};
 
   ~sph_ctx() {
     for (auto &e : ev)
@@ -898,6 +898,56 @@ int sph_step(sph_ctx *ctx, const sph_params *par, double *kernel_ms) {
     ctx->stats.last_force_ms = ms[4];
     if (kernel_ms)
       for (int k = 0; k < 6; ++k) kernel_ms[k] = ms[k];
+    return SPH_OK;
+  });
+}
+
+int sph_step_host(sph_ctx *ctx, void *const *recs, const sph_params *par, double *kernel_ms) {
+  return guarded(ctx, [&] {
+    if (!ctx->bound) throw ArgError{"sph_step_host before sph_bind"};
+    if (!par || !recs) throw ArgError{"null argument"};
+    const Params p = to_params(par);
+    const int path = SPH_PATH_AOS_BASELINE;
+    cudaEvent_t *e = ctx->ev + 6; // ev[6..14]
+    CK(cudaEventRecord(e[0], ctx->stream));
+    ctx->upload_full(recs);
+    CK(cudaEventRecord(e[1], ctx->stream));
+    ctx->sweep(SPH_KICK1, p, path);
+    CK(cudaEventRecord(e[2], ctx->stream));
+    ctx->sweep(SPH_DRIFT, p, path);
+    CK(cudaEventRecord(e[3], ctx->stream));
+    ctx->rebin();
+    CK(cudaEventRecord(e[4], ctx->stream));
+    ctx->sweep(SPH_DENSITY, p, path);
+    CK(cudaEventRecord(e[5], ctx->stream));
+    ctx->sweep(SPH_FORCE, p, path);
+    CK(cudaEventRecord(e[6], ctx->stream));
+    ctx->sweep(SPH_KICK2, p, path);
+    CK(cudaEventRecord(e[7], ctx->stream));
+    ctx->download_all(recs); // synchronises
+    CK(cudaEventRecord(e[8], ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    float ms[8];
+    for (int k = 0; k < 8; ++k) CK(cudaEventElapsedTime(&ms[k], e[k], e[k + 1]));
+    ctx->stats.last_density_ms = ms[4];
+    ctx->stats.last_force_ms = ms[5];
+    if (kernel_ms)
+      for (int k = 0; k < 8; ++k) kernel_ms[k] = ms[k];
+    return SPH_OK;
+  });
+}
+
+int sph_host_register(sph_ctx *ctx, void *base, uint64_t bytes) {
+  return guarded(ctx, [&] {
+    if (!base || !bytes) throw ArgError{"null range"};
+    CK(cudaHostRegister(base, (size_t)bytes, cudaHostRegisterDefault));
+    return SPH_OK;
+  });
+}
+
+int sph_host_unregister(sph_ctx *ctx, void *base) {
+  return guarded(ctx, [&] {
+    CK(cudaHostUnregister(base));
     return SPH_OK;
   });
 }

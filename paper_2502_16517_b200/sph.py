@@ -217,6 +217,23 @@ class Context:
         _check(self.h, self.lib.sph_step(self.h, C.byref(cp), ms.ctypes.data), "sph_step")
         return ms
 
+    def step_host(self, par: SphParams) -> np.ndarray:
+        """End-to-end step on the host records of the bound grid (H2D, step, D2H);
+        returns device ms for [H2D, kick1, drift, rebin, density, force, kick2, D2H]."""
+        self._need()
+        ms = np.zeros(8, np.float64)
+        cp = _cpar(par)
+        _check(self.h, self.lib.sph_step_host(self.h, self._ptrs.ctypes.data, C.byref(cp),
+                                              ms.ctypes.data), "sph_step_host")
+        return ms
+
+    def host_register(self, arr: np.ndarray) -> None:
+        _check(self.h, self.lib.sph_host_register(self.h, arr.ctypes.data, arr.nbytes),
+               "sph_host_register")
+
+    def host_unregister(self, arr: np.ndarray) -> None:
+        _check(self.h, self.lib.sph_host_unregister(self.h, arr.ctypes.data), "sph_host_unregister")
+
     def make_particles(self, n: int, ppc: int, seed: int) -> tuple[ParticleStore, CellGrid, SphParams]:
         """The reference IC computed on the device and left bound (continuous store)."""
         cp = _lib.SphParamsC()
