@@ -158,6 +158,31 @@ def test_exact_multistep_with_device_rebin(orc):
     assert recs.tobytes() == ref.tobytes()
 
 
+@pytest.mark.parametrize("layout", [DeviceLayout.Aos, DeviceLayout.Resident])
+def test_step_host_exact_matches_oracle(orc, layout):
+    """sph_step_host (host records in, host records out) == the oracle step, bytewise."""
+    n, ppc, seed = 3000, 64, 8
+    recs0, par = orc.make_particles(n, ppc, seed)
+    par = SphParams(dt=2e-3, gamma=par.gamma, cfl=par.cfl, grav=par.grav,
+                    target_wcount=par.target_wcount)
+    recs = recs0.copy()
+    ctx, store, grid = bound_ctx(recs, ppc, Numerics.Exact, layout)
+    ref = recs0.copy()
+    nx = grid.nx
+    with ctx:
+        ctx.host_register(recs)
+        for _ in range(2):
+            ctx.step_host(par)
+            for k in (KernelId.Kick1, KernelId.Drift):
+                cb, li = orc.build_grid(ref, nx)
+                orc.sweep(int(k), ref, nx, nx, 1.0 / nx, cb, li, par)
+            cb, li = orc.build_grid(ref, nx)
+            for k in (KernelId.Density, KernelId.Force, KernelId.Kick2):
+                orc.sweep(int(k), ref, nx, nx, 1.0 / nx, cb, li, par)
+        ctx.host_unregister(recs)
+    assert recs.tobytes() == ref.tobytes()
+
+
 @pytest.mark.parametrize("layout", LAYOUTS)
 def test_download_writes_only_aout(orc, ic_small, layout):
     """sph_download writes back only the kernel's A_out (+flags); a host-side edit of an
@@ -314,3 +339,17 @@ def test_errors_are_reported():
             ctx.sweep(KernelId.Density, SphParams())  # no bound grid
         with pytest.raises(pkg.SphError):
             ctx.set_numerics(7)
+
+
+def test_cpp_dropin_shim_against_reference():
+    """include/soaview_gpu.hpp linked with the unmodified reference in one binary
+    (oracle/_ref/shim_parity): byte-identical EXACT and within-tolerance FAST sweeps for
+    every kernel, both Path values, scattered and continuous stores."""
+    import os
+    import subprocess
+    exe = os.path.join(os.path.dirname(os.path.dirname(__file__)), "oracle", "_ref", "shim_parity")
+    if not os.path.exists(exe):
+        pytest.skip("oracle/_ref/shim_parity not built (needs /root/reference at build time)")
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
+    assert "[shim_parity] passed" in r.stdout
