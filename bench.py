@@ -187,11 +187,14 @@ def run_ours(args, rank, world, local):
     launches0 = ctx.launch_count()
     phase = np.zeros(6)
     den_eval = 0
+    round_ms = np.zeros(4)
     steps_ms = []
     with ClockSampler(local) as clk:
         for _ in range(args.steps):
             ms = ctx.step(par)
-            den_eval += ctx.stats()["density_pairs"]
+            st = ctx.stats()
+            den_eval += st["density_pairs"]
+            round_ms += np.array(st["density_round_ms"])
             phase += ms
             steps_ms.append(float(ms.sum()))
     ctx.synchronize()
@@ -214,6 +217,7 @@ def run_ours(args, rank, world, local):
         "workload_pairs_per_step": workload_pairs,
         "density_pairs_evaluated_per_step": den_eval / args.steps,
         "phase_ms": dict(zip(names, ph.round(4).tolist())),
+        "density_round_kernel_ms": (round_ms / args.steps).round(4).tolist(),
         "ic_seconds": round(t_ic, 2),
         "gpu_launches": launches,
         "gpu_launches_per_step": launches / args.steps,

@@ -80,6 +80,7 @@ typedef struct {
   int64_t density_failures;   /* last density sweep: particles that hit 30 rounds */
   int64_t force_pairs;        /* last force sweep: sum of nl*na */
   double last_density_ms, last_force_ms; /* device time of the pair kernels */
+  double density_round_ms[4];   /* last density sweep: kernel time of rounds 1-4 */
 } sph_stats;
 
 int sph_abi_version(void);

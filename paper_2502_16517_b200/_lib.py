@@ -30,7 +30,8 @@ class SphStatsC(C.Structure):
                 ("active_pairs", C.c_int64), ("density_pairs", C.c_int64),
                 ("density_updates", C.c_int64), ("density_rounds", C.c_int32),
                 ("pad0", C.c_int32), ("density_failures", C.c_int64), ("force_pairs", C.c_int64),
-                ("last_density_ms", C.c_double), ("last_force_ms", C.c_double)]
+                ("last_density_ms", C.c_double), ("last_force_ms", C.c_double),
+                ("density_round_ms", C.c_double * 4)]
 
 
 # Every exported symbol with its (restype, argtypes); tests check the library exports

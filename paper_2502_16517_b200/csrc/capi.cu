@@ -9,6 +9,7 @@
 // EXACT policy so the IC is byte-identical to the reference's.
 #include <algorithm>
 #include <atomic>
+#include <cstdlib>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -197,13 +198,15 @@ struct sph_ctx {
   bool soa_alloc = false;
   SoaMirror soa{};
 
-  DevBuf<int> cell_begin, cnt, pend_cnt, na_cell, ilist, pend_a, pend_b, host_idx, host_idx_tmp,
+  DevBuf<int> cell_begin, cnt, pend_cnt, pend_cnt2, na_cell, ilist, pend_a, pend_b, host_idx, host_idx_tmp,
       cellnew, vals, vals_sorted, scalars;
   DevBuf<long long> all_rank, all_rank_tmp, pairs_dev;
   DevBuf<unsigned long long> keys, keys_sorted;
   DevBuf<Item> items0, items_a, items_b;
   DevBuf<double> hcur, wc;
-  DevBuf<unsigned char> rounds;
+  DevBuf<unsigned char> rounds, again;
+  DevBuf<float4> boxes;
+  bool cull = true; // FAST density: spatial j order + chunk culling (env SPH_B200_CULL=0 disables)
   DevBuf<char> dense, cub_tmp;
   PinnedBuf h_stage, h_small;
   int n_items0 = 0;
@@ -217,9 +220,13 @@ struct sph_ctx {
   sph_stats stats{};
   int64_t launches = 0;
   cudaEvent_t ev[20]{};
+  cudaEvent_t rev[8]{};    // density round kernels (first four rounds)
+  double round_ms[4]{};
 
   ~sph_ctx() {
     for (auto &e : ev)
+      if (e) cudaEventDestroy(e);
+    for (auto &e : rev)
       if (e) cudaEventDestroy(e);
     if (stream) cudaStreamDestroy(stream);
     aos.release(); aos_tmp.release();
@@ -228,7 +235,7 @@ struct sph_ctx {
     f_udt.release(); f_c.release(); f_h.release(); f_wc.release(); f_rdh.release();
     f_rot.release(); f_div.release(); f_vsig.release(); f_hdt.release(); f_dtn.release();
     f_dbg0.release(); tmp1.release(); f_frozen.release(); f_moved.release(); f_flags.release();
-    tmp8.release(); cell_begin.release(); cnt.release(); pend_cnt.release(); na_cell.release();
+    tmp8.release(); cell_begin.release(); cnt.release(); pend_cnt.release(); pend_cnt2.release(); na_cell.release(); again.release();
     ilist.release(); pend_a.release(); pend_b.release(); host_idx.release();
     host_idx_tmp.release(); cellnew.release(); vals.release(); vals_sorted.release();
     scalars.release(); all_rank.release(); all_rank_tmp.release(); pairs_dev.release();
@@ -267,6 +274,8 @@ struct sph_ctx {
     cell_begin.ensure(nc + 1);
     cnt.ensure(nc);
     pend_cnt.ensure(nc);
+    pend_cnt2.ensure(nc);
+    again.ensure(N);
     na_cell.ensure(nc);
     ilist.ensure(N);
     pend_a.ensure(N);
@@ -335,32 +344,44 @@ struct sph_ctx {
     A.aos = aos.p;
     A.soa = soa;
     A.hcur = hcur.p;
-    A.pend_cnt = pend_cnt.p;
+    A.again = again.p;
     A.rounds_out = rounds.p;
     A.wc_out = wc.p;
+    if (!exact && !meanw && cull) {
+      boxes.ensure((size_t)n / 32 + (size_t)ncells + 2);
+      launch_chunk_boxes(boxes.p, ilist.p, aos.p, soa, use_aos, cell_begin.p, ncells, stream);
+      launched();
+      A.boxes = boxes.p;
+      A.jlist = ilist.p;
+    }
     const Item *items = items0.p;
     const int *list = ilist.p;
+    const int *cnt_cur = cnt.p; // entries of `list` per cell (round 0: every local)
     int nitems = n_items0;
-    int64_t pairs = active_pairs, pairs_total = 0, updates = 0;
+    int64_t pairs = active_pairs, pairs_total = 0;
     int max_round = 0;
+    for (double &v : round_ms) v = 0.0;
     int *pend_out = pend_a.p;
+    int *cnt_out = pend_cnt.p;
     Item *items_next = items_a.p;
     for (int r = 0; r < 30 && nitems > 0; ++r) {
       A.items = items;
       A.list = list;
       A.round = r;
-      A.pend_list = pend_out;
       if (meanw) {
         launch_density_exact(A, nitems, use_aos, true, stream);
         launched();
         break;
       }
-      CK(cudaMemsetAsync(pend_cnt.p, 0, sizeof(int) * ncells, stream));
+      if (r < 4) CK(cudaEventRecord(rev[2 * r], stream));
       if (exact) launch_density_exact(A, nitems, use_aos, false, stream);
       else launch_density_fast(A, nitems, use_aos, stream);
-      launch_make_items(items_next, scalars.p, pairs_dev.p, pend_cnt.p, cell_begin.p, na_cell.p,
+      if (r < 4) CK(cudaEventRecord(rev[2 * r + 1], stream));
+      launch_compact_pending(pend_out, cnt_out, list, cnt_cur, again.p, cell_begin.p, ncells,
+                             stream);
+      launch_make_items(items_next, scalars.p, pairs_dev.p, cnt_out, cell_begin.p, na_cell.p,
                         ncells, stream);
-      launched(2);
+      launched(3);
       pairs_total += pairs;
       max_round = r + 1;
       CK(cudaMemcpyAsync(h_small.p, scalars.p, sizeof(int), cudaMemcpyDeviceToHost, stream));
@@ -369,16 +390,23 @@ struct sph_ctx {
       CK(cudaStreamSynchronize(stream));
       nitems = *(int *)h_small.p;
       pairs = *(long long *)((char *)h_small.p + 8);
-      // next round reads what this one wrote
+      if (r < 4) {
+        float ms = 0;
+        CK(cudaEventElapsedTime(&ms, rev[2 * r], rev[2 * r + 1]));
+        round_ms[r] = ms;
+      }
+      // next round reads what this one produced
       items = items_next;
       list = pend_out;
+      cnt_cur = cnt_out;
       items_next = (items_next == items_a.p) ? items_b.p : items_a.p;
       pend_out = (pend_out == pend_a.p) ? pend_b.p : pend_a.p;
+      cnt_out = (cnt_out == pend_cnt.p) ? pend_cnt2.p : pend_cnt.p;
     }
     if (!meanw) {
       stats.density_pairs = pairs_total;
       stats.density_rounds = max_round;
-      (void)updates;
+      for (int k = 0; k < 4; ++k) stats.density_round_ms[k] = round_ms[k];
     }
   }
 
@@ -721,9 +749,11 @@ int sph_create(int device, sph_ctx **out) {
   sph_ctx *ctx = new (std::nothrow) sph_ctx;
   if (!ctx) return SPH_E_CUDA;
   ctx->device = device;
+  if (const char *e = std::getenv("SPH_B200_CULL")) ctx->cull = std::atoi(e) != 0;
   int r = guarded(ctx, [&] {
     CK(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
     for (auto &e : ctx->ev) CK(cudaEventCreate(&e));
+    for (auto &e : ctx->rev) CK(cudaEventCreate(&e));
     return SPH_OK;
   });
   if (r != SPH_OK) {

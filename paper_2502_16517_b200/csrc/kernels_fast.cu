@@ -300,8 +300,13 @@ void launch_density_fast(const DenArgs &a, int n_items, bool aos, cudaStream_t s
   DenArgs b = a;
   b.n_items = n_items;
   const int G = pair_grid(n_items), B = kWarpsPerCta * 32;
-  if (aos) density_round_kernel<FastPolicy, true, false><<<G, B, 0, s>>>(b);
-  else density_round_kernel<FastPolicy, false, false><<<G, B, 0, s>>>(b);
+  if (b.boxes && b.jlist) {
+    if (aos) density_cull_kernel<FastPolicy, true><<<G, B, 0, s>>>(b);
+    else density_cull_kernel<FastPolicy, false><<<G, B, 0, s>>>(b);
+  } else {
+    if (aos) density_round_kernel<FastPolicy, true, false><<<G, B, 0, s>>>(b);
+    else density_round_kernel<FastPolicy, false, false><<<G, B, 0, s>>>(b);
+  }
 }
 
 void launch_force_fast(const ForArgs &a, int n_items, bool aos, cudaStream_t s) {

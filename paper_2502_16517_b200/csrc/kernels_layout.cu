@@ -195,6 +195,53 @@ __global__ void spatial_order_kernel(int *__restrict__ ilist, const Particle *__
   }
 }
 
+// Bounding box (FP32, rounded outward) of every 32-chunk of each cell's ilist; one warp
+// per cell. Box index of chunk k of cell c: (cell_begin[c] >> 5) + c + k.
+__global__ void chunk_box_kernel(float4 *__restrict__ boxes, const int *__restrict__ ilist,
+                                 const Particle *__restrict__ aos, SoaMirror f, bool aos_src,
+                                 const int *__restrict__ cell_begin, int ncells) {
+  const int c = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (c >= ncells) return;
+  const int b = cell_begin[c], cnt = cell_begin[c + 1] - b;
+  for (int k = 0; k * 32 < cnt; ++k) {
+    const int q = k * 32 + lane;
+    const int sq = ilist[b + (q < cnt ? q : k * 32)];
+    const double2 x = aos_src ? *reinterpret_cast<const double2 *>(aos[sq].x) : f.x[sq];
+    float xlo = __double2float_rd(x.x), xhi = __double2float_ru(x.x);
+    float ylo = __double2float_rd(x.y), yhi = __double2float_ru(x.y);
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      xlo = fminf(xlo, __shfl_xor_sync(0xffffffffu, xlo, o));
+      xhi = fmaxf(xhi, __shfl_xor_sync(0xffffffffu, xhi, o));
+      ylo = fminf(ylo, __shfl_xor_sync(0xffffffffu, ylo, o));
+      yhi = fmaxf(yhi, __shfl_xor_sync(0xffffffffu, yhi, o));
+    }
+    if (lane == 0) boxes[(b >> 5) + c + k] = make_float4(xlo, ylo, xhi, yhi);
+  }
+}
+
+// Order-preserving compaction of the pending particles of each cell (one warp per cell):
+// out[cb[c] + k] = the k-th entry of in[cb[c] .. cb[c]+cnt_in[c]) whose again flag is set.
+__global__ void compact_pending_kernel(int *__restrict__ out, int *__restrict__ cnt_out,
+                                       const int *__restrict__ in, const int *__restrict__ cnt_in,
+                                       const unsigned char *__restrict__ again,
+                                       const int *__restrict__ cell_begin, int ncells) {
+  const int c = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (c >= ncells) return;
+  const int b = cell_begin[c], n = cnt_in[c];
+  int total = 0;
+  for (int k = 0; k < n; k += 32) {
+    const int q = k + lane;
+    const bool f = q < n && again[b + q];
+    const unsigned m = __ballot_sync(0xffffffffu, f);
+    if (f) out[b + total + __popc(m & ((1u << lane) - 1u))] = in[b + q];
+    total += __popc(m);
+  }
+  if (lane == 0) cnt_out[c] = total;
+}
+
 __global__ void cell_counts_kernel(int *__restrict__ na_cell, int *__restrict__ cnt,
                                    const int *__restrict__ cell_begin, int nx, int ny) {
   const int c = blockIdx.x * blockDim.x + threadIdx.x;
@@ -367,6 +414,19 @@ void launch_make_items(Item *items, int *n_items_out, long long *pairs_out, cons
                        const int *cell_begin, const int *na_cell, int ncells, cudaStream_t s) {
   make_items_kernel<<<1, 1024, 0, s>>>(items, n_items_out, pairs_out, cnt, cell_begin, na_cell,
                                        ncells);
+}
+void launch_chunk_boxes(float4 *boxes, const int *ilist, const Particle *aos, const SoaMirror &f,
+                        bool aos_src, const int *cell_begin, int ncells, cudaStream_t s) {
+  if (ncells > 0)
+    chunk_box_kernel<<<(ncells + 3) / 4, 128, 0, s>>>(boxes, ilist, aos, f, aos_src, cell_begin,
+                                                       ncells);
+}
+void launch_compact_pending(int *out, int *cnt_out, const int *in, const int *cnt_in,
+                            const unsigned char *again, const int *cell_begin, int ncells,
+                            cudaStream_t s) {
+  if (ncells > 0)
+    compact_pending_kernel<<<(ncells + 3) / 4, 128, 0, s>>>(out, cnt_out, in, cnt_in, again,
+                                                             cell_begin, ncells);
 }
 void launch_cell_counts(int *na_cell, int *cnt, const int *cell_begin, int nx, int ny,
                         cudaStream_t s) {

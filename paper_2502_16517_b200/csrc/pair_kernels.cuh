@@ -20,8 +20,9 @@
 //     (ilist: 8x8 sub-cell Morton bins), so the 32 lanes of a warp are neighbours and take
 //     the in-support branch together; the assignment does not affect any result.
 //   * density's smoothing-length iteration (kernels.cpp:184-192) runs as rounds: lanes that
-//     need another round append their particle to a per-cell pending list and the next
-//     launch processes only those, regrouped into full warps by cell.
+//     need another round raise a flag; an order-preserving per-cell compaction builds the
+//     next round's list (still in spatial order, so warps stay coherent) and the next launch
+//     processes only those particles, regrouped into full warps by cell.
 #pragma once
 #include "sph_common.cuh"
 
@@ -55,10 +56,11 @@ struct DenArgs {
   const Particle *aos;  // AoS source / destination (AOS instantiation)
   SoaMirror soa;        // SoA source / destination (SoA instantiation)
   double *hcur;         // per-slot h of the pending round
-  int *pend_cnt;        // per-cell pending counters (next round)
-  int *pend_list;       // next-round slots, cell c at [cell_begin[c], ...)
+  unsigned char *again; // per list position: 1 if the particle needs another round
   unsigned char *rounds_out; // optional per-slot round count (stats / parity analysis)
   double *wc_out;       // mean_wcount mode: per-slot neighbour sum (grid.cpp:36-50)
+  const int *jlist;     // culled FAST sweep: cell-major slots in spatial order (ilist)
+  const float4 *boxes;  // culled FAST sweep: bounding box of each 32-chunk of jlist
 };
 
 struct ForArgs {
@@ -105,6 +107,7 @@ template <> struct JSrc<false> {
 // Per-warp active-list layout: stencil cells, their slot ranges and prefix offsets.
 struct ActiveLayout {
   int n;          // stencil cells
+  int cell[9];    // stencil cell ids
   int na;         // active particles
   int pre[10];    // prefix of counts
   int base[9];    // first slot of each stencil cell
@@ -118,6 +121,7 @@ __device__ __forceinline__ void build_active(const Geom &g, int c, ActiveLayout 
   for (int k = 0; k < st.n; ++k) {
     int b = g.cell_begin[st.cell[k]], e = g.cell_begin[st.cell[k] + 1];
     L.base[k] = b;
+    L.cell[k] = st.cell[k];
     L.pre[k + 1] = L.pre[k] + (e - b);
     L.sx[k] = st.sx[k];
     L.sy[k] = st.sy[k];
@@ -219,10 +223,9 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, SPH_MINB_DEN) density_round
   }
   double hn = h;
   const int st = P::den_step(s, hn, A.target, A.h_max, A.round);
-  if (st == 0) { // Again: next round with hn
+  A.again[it.start + lane] = (unsigned char)(st == 0);
+  if (st == 0) { // Again: next round with hn (list compacted in order by compact_pending)
     A.hcur[slot] = hn;
-    const int pos = atomicAdd(&A.pend_cnt[it.cell], 1);
-    A.pend_list[A.g.cell_begin[it.cell] + pos] = slot;
     return;
   }
   double o[6]; // h, rho, wcount, rho_dh, rot_v, div_v
@@ -308,6 +311,109 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, SPH_MINB_FOR) force_kernel(
   } else {
     A.soa.a[slot] = make_double2(o[0], o[1]);
     A.soa.u_dt[slot] = o[2]; A.soa.v_sig[slot] = o[3]; A.soa.h_dt[slot] = o[4];
+  }
+}
+
+// ---------------------------------------------------------------------------------------
+// Culled density round (FAST numerics only; the j order is the spatial ilist order, which
+// the EXACT policy cannot use). The active list is walked per stencil cell in 32-particle
+// chunks of ilist; a chunk whose bounding box (precomputed, chunk_box_kernel) lies farther
+// than the warp's largest support radius 2.5 max(h_i) from the warp's own bounding box holds
+// no in-support pair for any lane (|x_i - x_j| < 2.5 h_i is necessary) and is skipped
+// without being loaded. Boxes are in FP32 with an absolute safety margin of 1e-6.
+// Chunk k of cell c has box index (cell_begin[c] >> 5) + c + k (unique, no scan needed).
+// ---------------------------------------------------------------------------------------
+__device__ __forceinline__ int chunk_box_index(int cell_begin_c, int c, int k) {
+  return (cell_begin_c >> 5) + c + k;
+}
+
+__device__ __forceinline__ float warp_min(float v) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) v = fminf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+__device__ __forceinline__ float warp_max(float v) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+template <class P, bool AOS>
+__global__ void __launch_bounds__(kWarpsPerCta * 32, SPH_MINB_DEN) density_cull_kernel(DenArgs A) {
+  __shared__ DenTile tiles[kWarpsPerCta];
+  __shared__ ActiveLayout lay[kWarpsPerCta];
+  const int w = warp_in_cta(), lane = lane_id();
+  const int item_idx = blockIdx.x * kWarpsPerCta + w;
+  if (item_idx >= A.n_items) return;
+  DenTile &T = tiles[w];
+  ActiveLayout &L = lay[w];
+  const Item it = A.items[item_idx];
+  if (lane == 0) build_active(A.g, it.cell, L);
+  JSrc<AOS> src;
+  if constexpr (AOS) src.p = A.aos; else src.f = A.soa;
+  const bool live = lane < it.count;
+  const int slot = A.list[it.start + (live ? lane : 0)];
+  const double2 xi = src.x(slot), vi = src.vp(slot);
+  const double mi = src.m(slot);
+  const double h = (A.round == 0) ? src.h(slot) : A.hcur[slot];
+  typename P::DI I = P::den_i(xi.x, xi.y, vi.x, vi.y, h);
+  typename P::DA s = P::den_zero();
+  // warp bounding box and reach (dead lanes carry lane 0's particle)
+  const float ixlo = warp_min((float)xi.x), ixhi = warp_max((float)xi.x);
+  const float iylo = warp_min((float)xi.y), iyhi = warp_max((float)xi.y);
+  const float reach = warp_max((float)(2.5 * h)) * (1.0f + 1e-5f) + 1e-6f;
+  const float reach2 = reach * reach;
+  __syncwarp();
+  const bool minimg = !A.g.use_shift;
+  for (int nb = 0; nb < L.n; ++nb) {
+    const int base = L.base[nb], cnt = L.pre[nb + 1] - L.pre[nb];
+    const float sx = (float)L.sx[nb], sy = (float)L.sy[nb];
+    const float4 *bx = A.boxes + chunk_box_index(base, L.cell[nb], 0);
+    for (int k = 0; k * kTJ < cnt; ++k) {
+      if (!minimg) {
+        const float4 b = bx[k]; // (xlo, ylo, xhi, yhi), same address for all lanes
+        const float gx = fmaxf(0.0f, fmaxf(b.x + sx - ixhi, ixlo - (b.z + sx)));
+        const float gy = fmaxf(0.0f, fmaxf(b.y + sy - iyhi, iylo - (b.w + sy)));
+        if (gx * gx + gy * gy > reach2) continue; // warp-uniform
+      }
+      const int q = k * kTJ + lane;
+      if (q < cnt) {
+        const int sj = A.jlist[base + q];
+        double2 rx = src.x(sj);
+        if (!minimg) { rx.x += L.sx[nb]; rx.y += L.sy[nb]; }
+        T.xy[lane] = rx;
+        T.vv[lane] = src.vp(sj);
+        T.m[lane] = src.m(sj);
+      } else {
+        T.xy[lane] = make_double2(kDummyX, kDummyX);
+        T.vv[lane] = make_double2(0.0, 0.0);
+        T.m[lane] = 0.0;
+      }
+      __syncwarp();
+      if (minimg) P::template den_tile<true>(I, T, s);
+      else P::template den_tile<false>(I, T, s);
+      __syncwarp();
+    }
+  }
+  if (!live) return;
+  double hn = h;
+  const int st = P::den_step(s, hn, A.target, A.h_max, A.round);
+  A.again[it.start + lane] = (unsigned char)(st == 0);
+  if (st == 0) {
+    A.hcur[slot] = hn;
+    return;
+  }
+  double o[6];
+  P::den_publish(s, h, mi, o);
+  if (A.rounds_out) A.rounds_out[slot] = (unsigned char)(A.round + 1);
+  if constexpr (AOS) {
+    Particle &pq = const_cast<Particle &>(A.aos[slot]);
+    pq.h = o[0]; pq.rho = o[1]; pq.wcount = o[2]; pq.rho_dh = o[3]; pq.rot_v = o[4]; pq.div_v = o[5];
+    if (st == 2) pq.flags += 1;
+  } else {
+    A.soa.h[slot] = o[0]; A.soa.rho[slot] = o[1]; A.soa.wcount[slot] = o[2];
+    A.soa.rho_dh[slot] = o[3]; A.soa.rot_v[slot] = o[4]; A.soa.div_v[slot] = o[5];
+    if (st == 2) A.soa.flags[slot] += 1;
   }
 }
 

@@ -40,6 +40,13 @@ void launch_spatial_order(int *ilist, const Particle *aos, const SoaMirror &f, b
 // out2[0] = n_items, out2[1] = pair count (sum cnt_c * na_c, int64 split in two ints)
 void launch_make_items(Item *items, int *n_items_out, long long *pairs_out, const int *cnt,
                        const int *cell_begin, const int *na_cell, int ncells, cudaStream_t s);
+// FP32 bounding boxes of the 32-chunks of each cell's ilist (culled FAST density)
+void launch_chunk_boxes(float4 *boxes, const int *ilist, const Particle *aos, const SoaMirror &f,
+                        bool aos_src, const int *cell_begin, int ncells, cudaStream_t s);
+// order-preserving per-cell compaction of the flagged (pending) list entries
+void launch_compact_pending(int *out, int *cnt_out, const int *in, const int *cnt_in,
+                            const unsigned char *again, const int *cell_begin, int ncells,
+                            cudaStream_t s);
 // per-cell active counts (sum of stencil cell counts) and per-cell local counts
 void launch_cell_counts(int *na_cell, int *cnt, const int *cell_begin, int nx, int ny,
                         cudaStream_t s);

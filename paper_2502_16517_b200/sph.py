@@ -257,7 +257,9 @@ class Context:
     def stats(self) -> dict:
         s = _lib.SphStatsC()
         _check(self.h, self.lib.sph_get_stats(self.h, C.byref(s)), "sph_get_stats")
-        return {name: getattr(s, name) for name, _ in s._fields_ if name != "pad0"}
+        out = {name: getattr(s, name) for name, _ in s._fields_ if name != "pad0"}
+        out["density_round_ms"] = list(s.density_round_ms)
+        return out
 
     def fp64_peak_tflops(self) -> float:
         v = C.c_double()
