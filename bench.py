@@ -225,7 +225,10 @@ def run_ours(args, rank, world, local):
     }
 
     # ---- e2e: the same step through the C-ABI on pinned host records ----
-    e2e_steps = max(1, args.e2e_steps)
+    e2e_steps = args.e2e_steps
+    if e2e_steps <= 0:
+        return _finish(out, ctx, store, grid, par, args, rank, world, ph, names, den_eval,
+                       workload_pairs)
     ctx.host_register(store.recs)
     try:
         ctx.step_host(par)  # warm-up
@@ -247,7 +250,11 @@ def run_ours(args, rank, world, local):
                   "api": "sph_step_host (C-ABI, host Particle records in and out)",
                   "device_ms": dict(zip(["h2d"] + names + ["d2h"],
                                         (dev / e2e_steps).round(3).tolist()))}
+    return _finish(out, ctx, store, grid, par, args, rank, world, ph, names, den_eval,
+                   workload_pairs)
 
+
+def _finish(out, ctx, store, grid, par, args, rank, world, ph, names, den_eval, workload_pairs):
     if rank == 0:
         fp64 = ctx.fp64_peak_tflops()
         peaks, src = load_peaks()
