@@ -42,6 +42,7 @@ sys.path.insert(0, ROOT)
 METRIC = "particle-pair interactions/sec (density+force)"
 UNIT = "pairs/s"
 F_IN_REF = (0.2236, 0.0804, 0.0089)  # SURVEY.md §8(d), reference IC at ppc 1024
+IC_KIND = {"uniform": 0, "clustered": 1}  # clustered = BASELINE config 3 (sph_b200.h)
 
 
 def flops_per_pair(f_in, f15, f05):
@@ -160,7 +161,9 @@ def pair_fractions(store, grid, ncells_sample=64, seed=1):
 
 
 def config_block(args, grid, world):
-    return {"workload": f"full SPH step, uniform 2-D box, n={args.n}, ppc={args.ppc}",
+    box = ("uniform 2-D box" if args.ic == "uniform" else
+           "clustered 2-D box (variable ppc: half uniform, half in 16 Gaussian clumps)")
+    return {"workload": f"full SPH step, {box}, n={args.n}, ppc={args.ppc}", "ic": args.ic,
             "n": args.n, "ppc": args.ppc, "nx": grid.nx if grid else None, "seed": args.seed,
             "dt": args.dt, "numerics": args.numerics, "layout": args.layout,
             "l2": "inputs larger than L2 (AoS mirror 0.57 GB + SoA mirror 0.44 GB at n=2^21)",
@@ -174,7 +177,7 @@ def run_ours(args, rank, world, local):
     ctx = pkg.Context(local, numerics=Numerics[args.numerics.capitalize()],
                       layout=DeviceLayout[args.layout.capitalize()])
     t0 = time.time()
-    store, grid, par = ctx.make_particles(args.n, args.ppc, args.seed)
+    store, grid, par = ctx.make_particles(args.n, args.ppc, args.seed, kind=IC_KIND[args.ic])
     t_ic = time.time() - t0
     par.dt = args.dt
     workload_pairs = 2 * ctx.stats()["active_pairs"]
@@ -325,7 +328,7 @@ def run_reference(args, rank, world, local):
     # IC: identical bytes to reference make_particles (which needs ~4 min on 8 cores at
     # 2^21); produced by the device IC path, outside the timed region.
     with pkg.Context(local) as ctx:
-        store, grid, par = ctx.make_particles(args.n, args.ppc, args.seed)
+        store, grid, par = ctx.make_particles(args.n, args.ppc, args.seed, kind=IC_KIND[args.ic])
     par.dt = args.dt
     stepper = ReferenceStepper(store.recs, args.ppc, par.as_array(),
                                sample_pairs=args.ref_sample_pairs)
@@ -365,6 +368,7 @@ def main():
     ap.add_argument("--seed", type=int, default=42)
     ap.add_argument("--dt", type=float, default=1e-4)
     ap.add_argument("--numerics", default="fast", choices=["fast", "exact"])
+    ap.add_argument("--ic", default="uniform", choices=["uniform", "clustered"])
     ap.add_argument("--layout", default="resident", choices=["resident", "aos", "convert"])
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--cpu-baseline", type=int, default=1)

@@ -145,6 +145,15 @@ int sph_step(sph_ctx *ctx, const sph_params *par, double *kernel_ms);
  * store (ParticleStore::all sorted by (cell, id)). par_out receives the calibrated params. */
 int sph_make_particles(sph_ctx *ctx, int64_t n, int ppc, uint64_t seed, sph_params *par_out);
 
+/* Initial-condition kinds for sph_make_particles_ex. UNIFORM is the reference's
+ * make_particles. CLUSTERED is the builder-defined variable-ppc IC of BASELINE config 3
+ * (the reference has none): the same RNG stream and pipeline, but half of the particles
+ * sit in 16 Gaussian clumps (sigma = 1 cell, centres drawn first, Irwin-Hall(12)
+ * deviates, wrapped with x - floor(x)); restated identically in oracle/sph_oracle.c. */
+enum { SPH_IC_UNIFORM = 0, SPH_IC_CLUSTERED = 1 };
+int sph_make_particles_ex(sph_ctx *ctx, int64_t n, int ppc, uint64_t seed, int kind,
+                          sph_params *par_out);
+
 /* Copy the mirror into a dense host array of n records in bound order (ParticleStore::all
  * order for sph_make_particles contexts). */
 int sph_read_records(sph_ctx *ctx, void *out_records);

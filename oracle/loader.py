@@ -66,6 +66,9 @@ class Oracle:
         lib.orc_mean_wcount.restype = C.c_double
         lib.orc_mean_wcount.argtypes = [_recp, C.c_int, C.c_int, _i64p, _i64p, C.c_int]
         lib.orc_make_proto.argtypes = [C.c_int64, C.c_int, C.c_uint64, _recp]
+        lib.orc_make_particles_kind.restype = C.c_int
+        lib.orc_make_particles_kind.argtypes = [C.c_int64, C.c_int, C.c_uint64, C.c_int, _recp,
+                                                _f64p, C.c_int]
         lib.orc_make_particles.restype = C.c_int
         lib.orc_make_particles.argtypes = [C.c_int64, C.c_int, C.c_uint64, _recp, _f64p, C.c_int]
         lib.orc_pair_stats.argtypes = [_recp, C.c_int, C.c_int, _i64p, _i64p, C.c_void_p, C.c_int,
@@ -105,11 +108,12 @@ class Oracle:
         self.lib.orc_make_proto(n, ppc, seed, out)
         return out
 
-    def make_particles(self, n: int, ppc: int, seed: int, threads=None):
-        """Continuous-layout IC: records sorted by (cell, id) + calibrated SphParams."""
+    def make_particles(self, n: int, ppc: int, seed: int, threads=None, kind: int = 0):
+        """Continuous-layout IC: records sorted by (cell, id) + calibrated SphParams.
+        kind 0 = reference uniform IC, 1 = clustered (variable ppc, BASELINE config 3)."""
         out = np.zeros(max(n, 1), PARTICLE_DTYPE)
         par = np.zeros(5, np.float64)
-        self.lib.orc_make_particles(n, ppc, seed, out, par, threads or self.threads)
+        self.lib.orc_make_particles_kind(n, ppc, seed, kind, out, par, threads or self.threads)
         return out, SphParams.from_array(par)
 
     def pair_stats(self, recs, nx, ny, cb, li, threads=None, cell_mask=None) -> np.ndarray:

@@ -431,18 +431,43 @@ static uint64_t mt64_next(mt64_t *s) {
 }
 static inline double unit_real(mt64_t *s) { return (double)(mt64_next(s) >> 11) * 0x1.0p-53; } /* grid.cpp:15-19 */
 
-/* Proto records of make_particles (grid.cpp:77-98), in id order. */
-void orc_make_proto(int64_t n, int ppc, uint64_t seed, orc_particle *out) {
+/* Proto records of make_particles (grid.cpp:77-98), in id order.
+ * kind 0: the reference IC (uniform random positions).
+ * kind 1: builder-defined clustered IC for variable ppc (BASELINE config 3; the reference
+ *         has no such generator): the same RNG stream, half the particles uniform, half in
+ *         16 Gaussian clumps (sigma = 1 cell) whose centres are drawn first; the normal
+ *         deviates are Irwin-Hall sums of 12 unit_real draws minus 6 (exact double
+ *         arithmetic, no libm) and positions wrap with x - floor(x). All other fields as
+ *         the reference. */
+void orc_make_proto_kind(int64_t n, int ppc, uint64_t seed, int kind, orc_particle *out) {
   mt64_t rng;
   mt64_seed(&rng, seed);
   if (n < 1) n = 1;
   double cell_size = 1.0 / orc_grid_nx(n, ppc);
   double h_warm = 0.8 * cell_size / SUPPORT;
+  double ccx[16], ccy[16];
+  const double sigma = 1.0 * cell_size;
+  if (kind == 1)
+    for (int k = 0; k < 16; ++k) {
+      ccx[k] = unit_real(&rng);
+      ccy[k] = unit_real(&rng);
+    }
   for (int64_t i = 0; i < n; ++i) {
     orc_particle *p = &out[i];
     memset(p, 0, sizeof *p);
-    p->x[0] = unit_real(&rng);
-    p->x[1] = unit_real(&rng);
+    if (kind == 1 && i >= n / 2) {
+      int k = (int)(mt64_next(&rng) % 16u);
+      double gx = 0.0, gy = 0.0;
+      for (int t = 0; t < 12; ++t) gx += unit_real(&rng);
+      for (int t = 0; t < 12; ++t) gy += unit_real(&rng);
+      double x0 = ccx[k] + sigma * (gx - 6.0);
+      double x1 = ccy[k] + sigma * (gy - 6.0);
+      p->x[0] = x0 - floor(x0);
+      p->x[1] = x1 - floor(x1);
+    } else {
+      p->x[0] = unit_real(&rng);
+      p->x[1] = unit_real(&rng);
+    }
     p->v[0] = (unit_real(&rng) * 2.0 - 1.0) * 0.05;
     p->v[1] = (unit_real(&rng) * 2.0 - 1.0) * 0.05;
     p->v_pred[0] = p->v[0];
@@ -454,6 +479,10 @@ void orc_make_proto(int64_t n, int ppc, uint64_t seed, orc_particle *out) {
     p->dt_next = 1.0e30;
     p->id = i;
   }
+}
+
+void orc_make_proto(int64_t n, int ppc, uint64_t seed, orc_particle *out) {
+  orc_make_proto_kind(n, ppc, seed, 0, out);
 }
 
 static int g_sort_nx;
@@ -473,10 +502,10 @@ static int cmp_cell_id(const void *a, const void *b) {
  * store.all order = sorted by (cell, id) (grid.cpp:117-132); par5 receives SphParams
  * defaults with the calibrated target_wcount. Values are layout-independent
  * (test_sph.cpp:138-149), so this also pins the scattered layout by id. */
-int orc_make_particles(int64_t n, int ppc, uint64_t seed, orc_particle *out, double *par5,
-                       int threads) {
+int orc_make_particles_kind(int64_t n, int ppc, uint64_t seed, int kind, orc_particle *out,
+                            double *par5, int threads) {
   if (n < 1) n = 1;
-  orc_make_proto(n, ppc, seed, out);
+  orc_make_proto_kind(n, ppc, seed, kind, out);
   int nx = orc_grid_nx(n, ppc);
   g_sort_nx = nx;
   qsort(out, (size_t)n, sizeof(orc_particle), cmp_cell_id);
@@ -500,6 +529,11 @@ int orc_make_particles(int64_t n, int ppc, uint64_t seed, orc_particle *out, dou
   free(cb);
   free(li);
   return 0;
+}
+
+int orc_make_particles(int64_t n, int ppc, uint64_t seed, orc_particle *out, double *par5,
+                       int threads) {
+  return orc_make_particles_kind(n, ppc, seed, 0, out, par5, threads);
 }
 
 /* Pair statistics of one density round at the records' current h:

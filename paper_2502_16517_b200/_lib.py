@@ -58,6 +58,8 @@ SIGNATURES = {
     "sph_host_register": (C.c_int, [_vp, _vp, C.c_uint64]),
     "sph_host_unregister": (C.c_int, [_vp, _vp]),
     "sph_make_particles": (C.c_int, [_vp, C.c_int64, C.c_int, C.c_uint64, C.POINTER(SphParamsC)]),
+    "sph_make_particles_ex": (C.c_int, [_vp, C.c_int64, C.c_int, C.c_uint64, C.c_int,
+                                        C.POINTER(SphParamsC)]),
     "sph_read_records": (C.c_int, [_vp, _vp]),
     "sph_get_stats": (C.c_int, [_vp, C.POINTER(SphStatsC)]),
     "sph_synchronize": (C.c_int, [_vp]),

@@ -202,6 +202,8 @@ struct sph_ctx {
       cellnew, vals, vals_sorted, scalars;
   DevBuf<long long> all_rank, all_rank_tmp, pairs_dev;
   DevBuf<unsigned long long> keys, keys_sorted;
+  DevBuf<unsigned> cost_key, cost_key_sorted;
+  DevBuf<int> cell_order, cell_order_in;
   DevBuf<Item> items0, items_a, items_b;
   DevBuf<double> hcur, wc;
   DevBuf<unsigned char> rounds, again;
@@ -239,7 +241,8 @@ struct sph_ctx {
     ilist.release(); pend_a.release(); pend_b.release(); host_idx.release();
     host_idx_tmp.release(); cellnew.release(); vals.release(); vals_sorted.release();
     scalars.release(); all_rank.release(); all_rank_tmp.release(); pairs_dev.release();
-    keys.release(); keys_sorted.release(); items0.release(); items_a.release();
+    keys.release(); keys_sorted.release(); cost_key.release(); cost_key_sorted.release();
+    cell_order.release(); cell_order_in.release(); items0.release(); items_a.release();
     items_b.release(); hcur.release(); wc.release(); rounds.release(); dense.release();
     cub_tmp.release(); h_stage.release(); h_small.release();
   }
@@ -298,11 +301,29 @@ struct sph_ctx {
 
   // Work list + derived per-cell data after the slot order changed.
   void rebuild_worklist() {
-    launch_cell_counts(na_cell.p, cnt.p, cell_begin.p, nx, ny, stream);
+    // per-cell counts, then the cell processing order: descending cost bucket, stable, so
+    // heavy cells (variable ppc) are scheduled first (LPT) while cells of similar cost keep
+    // their grid order (L2 reuse of shared neighbour cells)
+    cost_key.ensure(ncells);
+    cost_key_sorted.ensure(ncells);
+    cell_order_in.ensure(ncells);
+    cell_order.ensure(ncells);
+    launch_cell_counts(na_cell.p, cnt.p, cost_key.p, cell_order_in.p, cell_begin.p, nx, ny, stream);
+    {
+      size_t tb = 0;
+      CK(cub::DeviceRadixSort::SortPairsDescending(nullptr, tb, cost_key.p, cost_key_sorted.p,
+                                                   cell_order_in.p, cell_order.p, ncells, 0, 10,
+                                                   stream));
+      cub_tmp.ensure(tb);
+      CK(cub::DeviceRadixSort::SortPairsDescending(cub_tmp.p, tb, cost_key.p, cost_key_sorted.p,
+                                                   cell_order_in.p, cell_order.p, ncells, 0, 10,
+                                                   stream));
+      launched(2);
+    }
     const bool aos_src = !soa_ahead;
     launch_spatial_order(ilist.p, aos.p, soa, aos_src, cell_begin.p, ncells, nx, ny, stream);
-    launch_make_items(items0.p, scalars.p, pairs_dev.p, cnt.p, cell_begin.p, na_cell.p, ncells,
-                      stream);
+    launch_make_items(items0.p, scalars.p, pairs_dev.p, cnt.p, cell_begin.p, na_cell.p,
+                      cell_order.p, ncells, stream);
     launched(3);
     CK(cudaMemcpyAsync(h_small.p, scalars.p, sizeof(int), cudaMemcpyDeviceToHost, stream));
     CK(cudaMemcpyAsync((char *)h_small.p + 8, pairs_dev.p, sizeof(long long),
@@ -380,7 +401,7 @@ struct sph_ctx {
       launch_compact_pending(pend_out, cnt_out, list, cnt_cur, again.p, cell_begin.p, ncells,
                              stream);
       launch_make_items(items_next, scalars.p, pairs_dev.p, cnt_out, cell_begin.p, na_cell.p,
-                        ncells, stream);
+                        cell_order.p, ncells, stream);
       launched(3);
       pairs_total += pairs;
       max_round = r + 1;
@@ -983,22 +1004,45 @@ int sph_host_unregister(sph_ctx *ctx, void *base) {
 }
 
 int sph_make_particles(sph_ctx *ctx, int64_t n, int ppc, uint64_t seed, sph_params *par_out) {
+  return sph_make_particles_ex(ctx, n, ppc, seed, SPH_IC_UNIFORM, par_out);
+}
+
+int sph_make_particles_ex(sph_ctx *ctx, int64_t n, int ppc, uint64_t seed, int kind,
+                          sph_params *par_out) {
   return guarded(ctx, [&] {
     if (ppc <= 0) throw ArgError{"ppc must be positive"};
+    if (kind != SPH_IC_UNIFORM && kind != SPH_IC_CLUSTERED) throw ArgError{"unknown IC kind"};
     n = std::max<int64_t>(n, 1);
     if (n >= (1LL << 31)) throw ArgError{"n too large"};
-    // proto records in id order (grid.cpp:77-98)
+    // proto records in id order (grid.cpp:77-98); kind 1 = clustered (see sph_b200.h)
     Mt64 rng(seed);
     const int nx = grid_nx(n, ppc);
     const double cell_size = 1.0 / nx;
     const double h_warm = 0.8 * cell_size / kSupport;
+    const double sigma = 1.0 * cell_size;
+    double ccx[16], ccy[16];
+    if (kind == SPH_IC_CLUSTERED)
+      for (int k = 0; k < 16; ++k) {
+        ccx[k] = rng.unit();
+        ccy[k] = rng.unit();
+      }
     std::vector<Particle> proto((size_t)n);
     std::vector<int> cell((size_t)n);
     for (int64_t i = 0; i < n; ++i) {
       Particle &p = proto[(size_t)i];
       std::memset(&p, 0, sizeof p);
-      p.x[0] = rng.unit();
-      p.x[1] = rng.unit();
+      if (kind == SPH_IC_CLUSTERED && i >= n / 2) {
+        const int k = (int)(rng.next() % 16u);
+        double gx = 0.0, gy = 0.0;
+        for (int t = 0; t < 12; ++t) gx += rng.unit();
+        for (int t = 0; t < 12; ++t) gy += rng.unit();
+        const double x0 = ccx[k] + sigma * (gx - 6.0), x1 = ccy[k] + sigma * (gy - 6.0);
+        p.x[0] = x0 - std::floor(x0);
+        p.x[1] = x1 - std::floor(x1);
+      } else {
+        p.x[0] = rng.unit();
+        p.x[1] = rng.unit();
+      }
       p.v[0] = (rng.unit() * 2.0 - 1.0) * 0.05;
       p.v[1] = (rng.unit() * 2.0 - 1.0) * 0.05;
       p.v_pred[0] = p.v[0];

@@ -243,6 +243,7 @@ __global__ void compact_pending_kernel(int *__restrict__ out, int *__restrict__ 
 }
 
 __global__ void cell_counts_kernel(int *__restrict__ na_cell, int *__restrict__ cnt,
+                                   unsigned *__restrict__ cost_key, int *__restrict__ order,
                                    const int *__restrict__ cell_begin, int nx, int ny) {
   const int c = blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= nx * ny) return;
@@ -250,7 +251,12 @@ __global__ void cell_counts_kernel(int *__restrict__ na_cell, int *__restrict__ 
   int na = 0;
   for (int k = 0; k < st.n; ++k) na += cell_begin[st.cell[k] + 1] - cell_begin[st.cell[k]];
   na_cell[c] = na;
-  cnt[c] = cell_begin[c + 1] - cell_begin[c];
+  const int nl = cell_begin[c + 1] - cell_begin[c];
+  cnt[c] = nl;
+  // coarse cost bucket: 8 buckets per octave of nl * na (similar cells keep grid order)
+  const double cost = (double)nl * (double)na;
+  cost_key[c] = cost > 0.0 ? (unsigned)(8.0 * log2(cost)) + 1u : 0u;
+  order[c] = c;
 }
 
 // Single-CTA work-list builder: items for cell c = ceil(cnt[c] / kTI) chunks.
@@ -259,6 +265,7 @@ __global__ void __launch_bounds__(1024) make_items_kernel(Item *__restrict__ ite
                                                           const int *__restrict__ cnt,
                                                           const int *__restrict__ cell_begin,
                                                           const int *__restrict__ na_cell,
+                                                          const int *__restrict__ order,
                                                           int ncells) {
   typedef cub::BlockScan<int, 1024> Scan;
   typedef cub::BlockReduce<long long, 1024> Red;
@@ -269,16 +276,17 @@ __global__ void __launch_bounds__(1024) make_items_kernel(Item *__restrict__ ite
   long long pairs = 0;
   __syncthreads();
   for (int c0 = 0; c0 < ncells; c0 += 1024) {
-    const int c = c0 + threadIdx.x;
+    const int ci = c0 + threadIdx.x;
+    const int c = (ci < ncells && order) ? order[ci] : ci;
     int k = 0;
-    if (c < ncells) {
+    if (ci < ncells) {
       k = (cnt[c] + kTI - 1) / kTI;
       pairs += (long long)cnt[c] * na_cell[c];
     }
     int off, tot;
     Scan(ts).ExclusiveSum(k, off, tot);
     const int base = carry;
-    if (c < ncells) {
+    if (ci < ncells) {
       for (int q = 0; q < k; ++q) {
         Item it;
         it.cell = c;
@@ -411,9 +419,10 @@ void launch_spatial_order(int *ilist, const Particle *aos, const SoaMirror &f, b
     spatial_order_kernel<<<ncells, 256, 0, s>>>(ilist, aos, f, aos_src, cell_begin, nx, ny);
 }
 void launch_make_items(Item *items, int *n_items_out, long long *pairs_out, const int *cnt,
-                       const int *cell_begin, const int *na_cell, int ncells, cudaStream_t s) {
+                       const int *cell_begin, const int *na_cell, const int *order, int ncells,
+                       cudaStream_t s) {
   make_items_kernel<<<1, 1024, 0, s>>>(items, n_items_out, pairs_out, cnt, cell_begin, na_cell,
-                                       ncells);
+                                       order, ncells);
 }
 void launch_chunk_boxes(float4 *boxes, const int *ilist, const Particle *aos, const SoaMirror &f,
                         bool aos_src, const int *cell_begin, int ncells, cudaStream_t s) {
@@ -428,10 +437,12 @@ void launch_compact_pending(int *out, int *cnt_out, const int *in, const int *cn
     compact_pending_kernel<<<(ncells + 3) / 4, 128, 0, s>>>(out, cnt_out, in, cnt_in, again,
                                                              cell_begin, ncells);
 }
-void launch_cell_counts(int *na_cell, int *cnt, const int *cell_begin, int nx, int ny,
-                        cudaStream_t s) {
+void launch_cell_counts(int *na_cell, int *cnt, unsigned *cost_key, int *order,
+                        const int *cell_begin, int nx, int ny, cudaStream_t s) {
   const int nc = nx * ny;
-  if (nc > 0) cell_counts_kernel<<<(nc + 255) / 256, 256, 0, s>>>(na_cell, cnt, cell_begin, nx, ny);
+  if (nc > 0)
+    cell_counts_kernel<<<(nc + 255) / 256, 256, 0, s>>>(na_cell, cnt, cost_key, order, cell_begin,
+                                                         nx, ny);
 }
 void launch_rebin_keys(unsigned long long *keys, int *vals, int *cellnew, const Particle *aos,
                        const SoaMirror &f, bool aos_src, const long long *all_rank, int n, int nx,

@@ -38,8 +38,10 @@ void launch_spatial_order(int *ilist, const Particle *aos, const SoaMirror &f, b
                           const int *cell_begin, int ncells, int nx, int ny, cudaStream_t s);
 // work items from per-cell counts: items for cell c cover list[cell_begin[c] + k*kTI ...];
 // out2[0] = n_items, out2[1] = pair count (sum cnt_c * na_c, int64 split in two ints)
+// Items are emitted in `order` (cells sorted by descending cost bucket; may be null).
 void launch_make_items(Item *items, int *n_items_out, long long *pairs_out, const int *cnt,
-                       const int *cell_begin, const int *na_cell, int ncells, cudaStream_t s);
+                       const int *cell_begin, const int *na_cell, const int *order, int ncells,
+                       cudaStream_t s);
 // FP32 bounding boxes of the 32-chunks of each cell's ilist (culled FAST density)
 void launch_chunk_boxes(float4 *boxes, const int *ilist, const Particle *aos, const SoaMirror &f,
                         bool aos_src, const int *cell_begin, int ncells, cudaStream_t s);
@@ -48,8 +50,9 @@ void launch_compact_pending(int *out, int *cnt_out, const int *in, const int *cn
                             const unsigned char *again, const int *cell_begin, int ncells,
                             cudaStream_t s);
 // per-cell active counts (sum of stencil cell counts) and per-cell local counts
-void launch_cell_counts(int *na_cell, int *cnt, const int *cell_begin, int nx, int ny,
-                        cudaStream_t s);
+// also writes a per-cell cost bucket key (8 per octave of nl*na) and order = identity
+void launch_cell_counts(int *na_cell, int *cnt, unsigned *cost_key, int *order,
+                        const int *cell_begin, int nx, int ny, cudaStream_t s);
 // rebin helpers
 void launch_rebin_keys(unsigned long long *keys, int *vals, int *cellnew, const Particle *aos,
                        const SoaMirror &f, bool aos_src, const long long *all_rank, int n, int nx,

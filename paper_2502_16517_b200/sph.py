@@ -234,11 +234,13 @@ class Context:
     def host_unregister(self, arr: np.ndarray) -> None:
         _check(self.h, self.lib.sph_host_unregister(self.h, arr.ctypes.data), "sph_host_unregister")
 
-    def make_particles(self, n: int, ppc: int, seed: int) -> tuple[ParticleStore, CellGrid, SphParams]:
-        """The reference IC computed on the device and left bound (continuous store)."""
+    def make_particles(self, n: int, ppc: int, seed: int,
+                       kind: int = 0) -> tuple[ParticleStore, CellGrid, SphParams]:
+        """The reference IC computed on the device and left bound (continuous store).
+        kind 0 = reference uniform IC, 1 = clustered variable-ppc IC (BASELINE config 3)."""
         cp = _lib.SphParamsC()
-        _check(self.h, self.lib.sph_make_particles(self.h, n, ppc, seed, C.byref(cp)),
-               "sph_make_particles")
+        _check(self.h, self.lib.sph_make_particles_ex(self.h, n, ppc, seed, int(kind),
+                                                      C.byref(cp)), "sph_make_particles_ex")
         n = max(n, 1)
         recs = np.zeros(n, PARTICLE_DTYPE)
         _check(self.h, self.lib.sph_read_records(self.h, recs.ctypes.data), "sph_read_records")

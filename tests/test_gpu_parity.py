@@ -66,6 +66,24 @@ def test_device_ic_is_byte_identical(orc, n, ppc, seed):
     assert par.target_wcount == rpar.target_wcount
 
 
+@pytest.mark.parametrize("n,ppc,seed", [(6000, 64, 3), (40000, 256, 5)])
+def test_device_clustered_ic_matches_oracle(orc, n, ppc, seed):
+    """The variable-ppc IC (BASELINE config 3) on the device == its oracle restatement."""
+    with pkg.Context(0) as ctx:
+        store, grid, par = ctx.make_particles(n, ppc, seed, kind=1)
+    ref, rpar = orc.make_particles(n, ppc, seed, kind=1)
+    assert store.recs.tobytes() == ref.tobytes()
+    assert par.target_wcount == rpar.target_wcount
+    counts = np.diff(grid.cell_begin)
+    assert counts.max() > 1.5 * counts.mean()  # genuinely variable ppc
+
+
+@pytest.mark.parametrize("k", [KernelId.Density, KernelId.Force])
+def test_fast_sweep_clustered(orc, k):
+    recs0, par = orc.make_particles(40000, 256, 5, kind=1)
+    _check_fast(orc, recs0, par, 256, DeviceLayout.Resident, k)
+
+
 @pytest.mark.parametrize("layout", LAYOUTS)
 @pytest.mark.parametrize("k", KERNELS)
 def test_exact_sweep_bitwise(orc, ic_small, k, layout):

@@ -159,3 +159,16 @@ def test_isolated_and_pair_known_answers(orc):
     assert r["rho"][0] == r["rho"][1] > 0
     orc.sweep(1, r, nx, nx, 1.0 / nx, cb, li, par)
     assert r["a"][0, 0] == -r["a"][1, 0] != 0.0 and r["v_sig"][0] == r["v_sig"][1]
+
+
+def test_clustered_ic_is_variable_and_deterministic(orc):
+    """Builder-defined variable-ppc IC (BASELINE config 3): deterministic per seed, the
+    first half identical in distribution to the reference IC, strong ppc contrast."""
+    a, pa = orc.make_particles(20000, 64, 3, kind=1)
+    b, pb = orc.make_particles(20000, 64, 3, kind=1)
+    assert a.tobytes() == b.tobytes() and pa == pb
+    nx = orc.grid_nx(20000, 64)
+    cb, _ = orc.build_grid(a.copy(), nx)
+    c = np.diff(cb)
+    assert c.max() > 2.5 * c.mean() and c.sum() == 20000
+    assert np.all(a["x"] >= 0.0) and np.all(a["x"] <= 1.0)
