@@ -101,6 +101,11 @@ int sph_set_layout(sph_ctx *ctx, int layout);
 int sph_bind(sph_ctx *ctx, void *const *recs, const int64_t *cell_begin, int nx, int ny,
              double cell_size, const int64_t *all_rank);
 
+/* Domain decomposition: sweeps compute only the cells with owned[c] != 0 (NULL = all);
+ * particles of other bound cells (halo) still appear in the active lists but are not
+ * updated by density / force. Takes effect immediately and survives rebins. */
+int sph_set_owned_cells(sph_ctx *ctx, const uint8_t *owned);
+
 /* Re-upload all records (host mutated them); recs in the bound order. */
 int sph_upload(sph_ctx *ctx, void *const *recs);
 

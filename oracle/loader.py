@@ -63,6 +63,9 @@ class Oracle:
         lib.orc_sweep.restype = C.c_int
         lib.orc_sweep.argtypes = [C.c_int, _recp, C.c_int, C.c_int, C.c_double, _i64p, _i64p,
                                   _f64p, C.c_int, C.c_void_p]
+        lib.orc_sweep_masked.restype = C.c_int
+        lib.orc_sweep_masked.argtypes = [C.c_int, _recp, C.c_int, C.c_int, C.c_double, _i64p,
+                                         _i64p, _f64p, C.c_int, C.c_void_p, C.c_void_p]
         lib.orc_mean_wcount.restype = C.c_double
         lib.orc_mean_wcount.argtypes = [_recp, C.c_int, C.c_int, _i64p, _i64p, C.c_int]
         lib.orc_make_proto.argtypes = [C.c_int64, C.c_int, C.c_uint64, _recp]
@@ -99,6 +102,12 @@ class Oracle:
         rp = rounds.ctypes.data_as(C.c_void_p) if rounds is not None else None
         self.lib.orc_sweep(int(kernel), recs, nx, ny, cell_size, cb, li, _par(par),
                            threads or self.threads, rp)
+
+    def sweep_masked(self, kernel: int, recs, nx, ny, cell_size, cb, li, par, cell_mask,
+                     threads=None) -> None:
+        m = np.ascontiguousarray(cell_mask, np.uint8)
+        self.lib.orc_sweep_masked(int(kernel), recs, nx, ny, cell_size, cb, li, _par(par),
+                                  threads or self.threads, None, m.ctypes.data)
 
     def mean_wcount(self, recs, nx, ny, cb, li, threads=None) -> float:
         return self.lib.orc_mean_wcount(recs, nx, ny, cb, li, threads or self.threads)

@@ -319,22 +319,26 @@ void orc_kick2_one(orc_particle *p, const double *par5) {
   p->h_dt = 0.0;
 }
 
-/* One sweep of kernel k over all cells (run_sweep, kernels.cpp:861-872).
+/* One sweep of kernel k over all cells, or over the cells with cell_mask[c] != 0 (the owned
+ * cells of a domain-decomposition rank; other cells still feed the active lists)
+ * (run_sweep, kernels.cpp:861-872).
  * kernel: 0 density, 1 force, 2 drift, 3 kick1, 4 kick2 (KernelId order, kernels.hpp:9).
  * rounds_out: optional per-record h-round counts (density only). Returns 0. */
-int orc_sweep(int kernel, orc_particle *recs, int nx, int ny, double cell_size,
-              const int64_t *cell_begin, const int64_t *local_idx, const double *par5,
-              int threads, int32_t *rounds_out) {
+int orc_sweep_masked(int kernel, orc_particle *recs, int nx, int ny, double cell_size,
+                     const int64_t *cell_begin, const int64_t *local_idx, const double *par5,
+                     int threads, int32_t *rounds_out, const uint8_t *cell_mask) {
   grid_t g = {recs, nx, ny, cell_size, cell_begin, local_idx};
   int nc = nx * ny;
   if (kernel >= 2) {
-    int64_t n = cell_begin[nc];
-#pragma omp parallel for schedule(static) num_threads(threads > 0 ? threads : 1)
-    for (int64_t t = 0; t < n; ++t) {
+#pragma omp parallel for schedule(dynamic, 16) num_threads(threads > 0 ? threads : 1)
+    for (int c = 0; c < nc; ++c) {
+      if (cell_mask && !cell_mask[c]) continue;
+      for (int64_t t = cell_begin[c]; t < cell_begin[c + 1]; ++t) {
       orc_particle *p = &recs[local_idx[t]];
       if (kernel == 2) orc_drift_one(p, par5);
       else if (kernel == 3) orc_kick1_one(p, par5);
       else orc_kick2_one(p, par5);
+      }
     }
     return 0;
   }
@@ -347,6 +351,7 @@ int orc_sweep(int kernel, orc_particle *recs, int nx, int ny, double cell_size,
 #pragma omp for schedule(dynamic, 1)
     for (int c = 0; c < nc; ++c) {
       if (cell_begin[c + 1] == cell_begin[c]) continue; /* kernels.cpp:548 */
+      if (cell_mask && !cell_mask[c]) continue;         /* not owned (decomposition) */
       int64_t na = active_of(&g, c, act);
       if (kernel == 0) density_cell(&g, c, act, na, target, h_max, rounds_out);
       else force_cell(&g, c, act, na, grav);
@@ -354,6 +359,13 @@ int orc_sweep(int kernel, orc_particle *recs, int nx, int ny, double cell_size,
     free(act);
   }
   return 0;
+}
+
+int orc_sweep(int kernel, orc_particle *recs, int nx, int ny, double cell_size,
+              const int64_t *cell_begin, const int64_t *local_idx, const double *par5,
+              int threads, int32_t *rounds_out) {
+  return orc_sweep_masked(kernel, recs, nx, ny, cell_size, cell_begin, local_idx, par5, threads,
+                          rounds_out, NULL);
 }
 
 /* mean_wcount, grid.cpp:31-54: per-particle sums in parallel, total summed in order. */

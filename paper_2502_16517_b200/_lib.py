@@ -45,6 +45,7 @@ SIGNATURES = {
     "sph_set_numerics": (C.c_int, [_vp, C.c_int]),
     "sph_set_layout": (C.c_int, [_vp, C.c_int]),
     "sph_bind": (C.c_int, [_vp, _vp, _vp, C.c_int, C.c_int, C.c_double, _vp]),
+    "sph_set_owned_cells": (C.c_int, [_vp, _vp]),
     "sph_upload": (C.c_int, [_vp, _vp]),
     "sph_download": (C.c_int, [_vp, _vp]),
     "sph_download_all": (C.c_int, [_vp, _vp]),

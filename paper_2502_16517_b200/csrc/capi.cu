@@ -203,6 +203,8 @@ struct sph_ctx {
   DevBuf<long long> all_rank, all_rank_tmp, pairs_dev;
   DevBuf<unsigned long long> keys, keys_sorted;
   DevBuf<unsigned> cost_key, cost_key_sorted;
+  DevBuf<unsigned char> owned;
+  bool has_owned = false;
   DevBuf<int> cell_order, cell_order_in;
   DevBuf<Item> items0, items_a, items_b;
   DevBuf<double> hcur, wc;
@@ -244,7 +246,7 @@ struct sph_ctx {
     keys.release(); keys_sorted.release(); cost_key.release(); cost_key_sorted.release();
     cell_order.release(); cell_order_in.release(); items0.release(); items_a.release();
     items_b.release(); hcur.release(); wc.release(); rounds.release(); dense.release();
-    cub_tmp.release(); h_stage.release(); h_small.release();
+    cub_tmp.release(); h_stage.release(); h_small.release(); owned.release();
   }
 
   Geom geom() const {
@@ -309,6 +311,10 @@ struct sph_ctx {
     cell_order_in.ensure(ncells);
     cell_order.ensure(ncells);
     launch_cell_counts(na_cell.p, cnt.p, cost_key.p, cell_order_in.p, cell_begin.p, nx, ny, stream);
+    if (has_owned) {
+      launch_mask_counts(cnt.p, cost_key.p, owned.p, ncells, stream); // halo cells: no items
+      launched();
+    }
     {
       size_t tb = 0;
       CK(cub::DeviceRadixSort::SortPairsDescending(nullptr, tb, cost_key.p, cost_key_sorted.p,
@@ -816,6 +822,21 @@ int sph_bind(sph_ctx *ctx, void *const *recs, const int64_t *cell_begin, int nx,
   return guarded(ctx, [&] {
     if (!cell_begin || (!recs && cell_begin[(size_t)nx * ny] > 0)) throw ArgError{"null argument"};
     ctx->bind(recs, cell_begin, nx, ny, cell_size, all_rank);
+    return SPH_OK;
+  });
+}
+
+int sph_set_owned_cells(sph_ctx *ctx, const uint8_t *owned) {
+  return guarded(ctx, [&] {
+    if (!ctx->bound) throw ArgError{"sph_set_owned_cells before sph_bind"};
+    if (owned) {
+      ctx->owned.ensure(ctx->ncells);
+      CK(cudaMemcpyAsync(ctx->owned.p, owned, ctx->ncells, cudaMemcpyHostToDevice, ctx->stream));
+      ctx->has_owned = true;
+    } else {
+      ctx->has_owned = false;
+    }
+    ctx->rebuild_worklist();
     return SPH_OK;
   });
 }

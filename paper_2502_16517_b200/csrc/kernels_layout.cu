@@ -430,6 +430,18 @@ void launch_chunk_boxes(float4 *boxes, const int *ilist, const Particle *aos, co
     chunk_box_kernel<<<(ncells + 3) / 4, 128, 0, s>>>(boxes, ilist, aos, f, aos_src, cell_begin,
                                                        ncells);
 }
+__global__ void mask_counts_kernel(int *cnt, unsigned *cost_key, const unsigned char *owned,
+                                   int ncells) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c < ncells && !owned[c]) {
+    cnt[c] = 0;
+    cost_key[c] = 0u;
+  }
+}
+void launch_mask_counts(int *cnt, unsigned *cost_key, const unsigned char *owned, int ncells,
+                        cudaStream_t s) {
+  if (ncells > 0) mask_counts_kernel<<<(ncells + 255) / 256, 256, 0, s>>>(cnt, cost_key, owned, ncells);
+}
 void launch_compact_pending(int *out, int *cnt_out, const int *in, const int *cnt_in,
                             const unsigned char *again, const int *cell_begin, int ncells,
                             cudaStream_t s) {

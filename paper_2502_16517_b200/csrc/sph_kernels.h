@@ -45,6 +45,9 @@ void launch_make_items(Item *items, int *n_items_out, long long *pairs_out, cons
 // FP32 bounding boxes of the 32-chunks of each cell's ilist (culled FAST density)
 void launch_chunk_boxes(float4 *boxes, const int *ilist, const Particle *aos, const SoaMirror &f,
                         bool aos_src, const int *cell_begin, int ncells, cudaStream_t s);
+// zero the work counts of cells that are not owned (domain decomposition halo)
+void launch_mask_counts(int *cnt, unsigned *cost_key, const unsigned char *owned, int ncells,
+                        cudaStream_t s);
 // order-preserving per-cell compaction of the flagged (pending) list entries
 void launch_compact_pending(int *out, int *cnt_out, const int *in, const int *cnt_in,
                             const unsigned char *again, const int *cell_begin, int ncells,

@@ -1,0 +1,260 @@
+"""Spatial domain decomposition of the SPH step across ranks.
+
+The reference has no decomposition; this is the B200 build's multi-GPU path,
+designed so that EXACT results on k ranks equal 1 rank equal the CPU reference:
+
+* ``SlabDecomposition``: the periodic nx x ny cell grid is cut into slabs of cell columns,
+  one per rank. A rank owns the particles of its columns and keeps a one-column halo on
+  each side (torus wrap). Halo particles keep their GLOBAL cell and ParticleStore::all
+  rank, so every owned cell sees exactly the reference's active list (build_grid order,
+  grid.cpp:152-182).
+* ``DistributedSim.step``: kick1 + drift on owned particles -> migration of particles that
+  left the slab (272-B records to their new owner) -> halo exchange of boundary-column
+  records -> density on owned cells -> halo refresh (density changed rho, which force
+  reads for active particles, kernels.cpp:443-456) -> force on owned cells -> kick2.
+  Exchanges are point-to-point with the two slab neighbours (``torch.distributed``: NCCL
+  on GPUs, gloo in the CPU tests).
+* Compute goes through a backend: ``DeviceBackend`` (the C-ABI, one context per rank) in
+  production; tests plug in the CPU oracle to check the host-side logic on any machine.
+"""
+from __future__ import annotations
+
+import numpy as np
+
+from .particle import PARTICLE_DTYPE, RECORD_SIZE, DeviceLayout, KernelId, Numerics, SphParams
+
+DENSITY, FORCE, DRIFT, KICK1, KICK2 = (int(k) for k in (KernelId.Density, KernelId.Force,
+                                                         KernelId.Drift, KernelId.Kick1,
+                                                         KernelId.Kick2))
+
+
+def cell_of(recs: np.ndarray, nx: int, ny: int) -> np.ndarray:
+    """build_grid's cell index (grid.cpp:153-155): clamp(floor(x*nx)), row-major."""
+    x = recs["x"]
+    cx = np.clip(np.floor(x[:, 0] * nx).astype(np.int64), 0, nx - 1)
+    cy = np.clip(np.floor(x[:, 1] * nx).astype(np.int64), 0, ny - 1)
+    return cy * nx + cx
+
+
+class SlabDecomposition:
+    """Slabs of cell columns of the periodic nx x ny grid; rank r owns [c0_r, c1_r)."""
+
+    def __init__(self, nx: int, ny: int, world: int, rank: int):
+        if world < 1 or not 0 <= rank < world:
+            raise ValueError("bad world / rank")
+        if world > 1 and nx < 2 * world:
+            raise ValueError("each rank needs at least two cell columns")
+        self.nx, self.ny, self.world, self.rank = nx, ny, world, rank
+        self.bounds = [(r * nx) // world for r in range(world + 1)]
+        self.col_owner = np.empty(nx, np.int64)
+        for r in range(world):
+            self.col_owner[self.bounds[r]:self.bounds[r + 1]] = r
+
+    def owned_cols(self, r: int | None = None) -> np.ndarray:
+        r = self.rank if r is None else r
+        return np.arange(self.bounds[r], self.bounds[r + 1])
+
+    def halo_cols(self, r: int | None = None) -> np.ndarray:
+        r = self.rank if r is None else r
+        if self.world == 1:
+            return np.zeros(0, np.int64)
+        c0, c1 = self.bounds[r], self.bounds[r + 1]
+        h = {(c0 - 1) % self.nx, c1 % self.nx}
+        return np.array(sorted(c for c in h if self.col_owner[c] != r), np.int64)
+
+    def neighbours(self) -> list[int]:
+        return sorted({int(self.col_owner[c]) for c in self.halo_cols()} - {self.rank})
+
+    def cells_mask(self, cols: np.ndarray) -> np.ndarray:
+        m = np.zeros(self.nx, bool)
+        m[cols] = True
+        return np.tile(m, self.ny)
+
+    def owned_cells_mask(self) -> np.ndarray:
+        return self.cells_mask(self.owned_cols())
+
+    def send_cols(self, q: int) -> np.ndarray:
+        """My owned columns that lie in rank q's halo."""
+        return np.intersect1d(self.owned_cols(), self.halo_cols(q))
+
+
+class Exchanger:
+    """Neighbour point-to-point exchange of (records, all_rank) sets."""
+
+    def __init__(self, group=None, device=None):
+        import torch.distributed as dist
+        self.dist = dist
+        self.group = group
+        self.device = device  # None: CPU tensors (gloo); else a torch.device (NCCL)
+
+    def exchange(self, send: dict[int, tuple[np.ndarray, np.ndarray]], peers: list[int]):
+        import torch
+        dist = self.dist
+        dev = self.device or torch.device("cpu")
+        cnt_in = {q: torch.zeros(1, dtype=torch.int64, device=dev) for q in peers}
+        reqs = []
+        for q in peers:
+            n = len(send.get(q, (np.zeros(0, PARTICLE_DTYPE),))[0])
+            reqs.append(dist.isend(torch.tensor([n], dtype=torch.int64, device=dev), q, group=self.group))
+            reqs.append(dist.irecv(cnt_in[q], q, group=self.group))
+        for r in reqs:
+            r.wait()
+        reqs, bufs = [], {}
+        keep = []
+        for q in peers:
+            recs, ranks = send.get(q, (np.zeros(0, PARTICLE_DTYPE), np.zeros(0, np.int64)))
+            if len(recs):
+                t = torch.from_numpy(np.ascontiguousarray(recs).view(np.uint8).reshape(-1)).to(dev)
+                tr = torch.from_numpy(np.ascontiguousarray(ranks, np.int64)).to(dev)
+                keep += [t, tr]
+                reqs.append(dist.isend(t, q, group=self.group))
+                reqs.append(dist.isend(tr, q, group=self.group))
+            m = int(cnt_in[q].item())
+            if m:
+                b = torch.empty(m * RECORD_SIZE, dtype=torch.uint8, device=dev)
+                br = torch.empty(m, dtype=torch.int64, device=dev)
+                bufs[q] = (b, br)
+                reqs.append(dist.irecv(b, q, group=self.group))
+                reqs.append(dist.irecv(br, q, group=self.group))
+        for r in reqs:
+            r.wait()
+        out = {}
+        for q in peers:
+            if q in bufs:
+                b, br = bufs[q]
+                out[q] = (b.cpu().numpy().view(PARTICLE_DTYPE).copy(), br.cpu().numpy().copy())
+            else:
+                out[q] = (np.zeros(0, PARTICLE_DTYPE), np.zeros(0, np.int64))
+        return out
+
+
+class DeviceBackend:
+    """Sweeps through the C-ABI on this rank's GPU (host-staged: records are bound per call)."""
+
+    def __init__(self, device: int = 0, numerics: Numerics = Numerics.Fast):
+        from .sph import Context
+        self.ctx = Context(device, numerics=numerics, layout=DeviceLayout.Resident)
+
+    def _bind(self, recs, ranks, nx, ny, mask=None):
+        from .sph import CellGrid, ParticleStore
+        store = ParticleStore(recs, np.arange(len(recs), dtype=np.int64))
+        if mask is None:  # linear kernels: any grid enumerating every particle once
+            grid = CellGrid(1, 1, 1.0, np.array([0, len(recs)], np.int64),
+                            np.arange(len(recs), dtype=np.int64), store,
+                            all_rank=np.asarray(ranks, np.int64))
+        else:
+            c = cell_of(recs, nx, ny)
+            cb = np.zeros(nx * ny + 1, np.int64)
+            np.cumsum(np.bincount(c, minlength=nx * ny), out=cb[1:])
+            grid = CellGrid(nx, ny, 1.0 / nx, cb, np.arange(len(recs), dtype=np.int64), store,
+                            all_rank=np.asarray(ranks, np.int64))
+        self.ctx.bind(grid)
+        if mask is not None:
+            self.ctx.set_owned_cells(mask)
+
+    def linear(self, kernel: int, recs, ranks, par):
+        if len(recs):
+            self._bind(recs, ranks, 1, 1)
+            self.ctx.run_sweep(KernelId(kernel), par)
+
+    def pair(self, kernel: int, recs, ranks, nx, ny, owned_mask, par):
+        """recs must be sorted by (cell, all_rank)."""
+        if len(recs):
+            self._bind(recs, ranks, nx, ny, owned_mask)
+            self.ctx.run_sweep(KernelId(kernel), par)
+
+    def close(self):
+        self.ctx.close()
+
+
+def sort_local(recs, ranks, nx, ny):
+    """(cell, all_rank) order = build_grid's list order for the global store."""
+    c = cell_of(recs, nx, ny)
+    order = np.lexsort((ranks, c))
+    return recs[order], ranks[order]
+
+
+class DistributedSim:
+    """One rank of the slab-decomposed leapfrog step."""
+
+    def __init__(self, decomp: SlabDecomposition, recs: np.ndarray, ranks: np.ndarray,
+                 backend, exchanger: Exchanger | None):
+        self.d = decomp
+        self.own = np.ascontiguousarray(recs)
+        self.ranks = np.ascontiguousarray(ranks, np.int64)
+        self.be = backend
+        self.ex = exchanger
+        self.last = {}
+
+    @staticmethod
+    def split_global(recs: np.ndarray, decomp: SlabDecomposition):
+        """This rank's owned share of a global store (records in ParticleStore::all order)."""
+        c = cell_of(recs, decomp.nx, decomp.ny)
+        mine = decomp.col_owner[c % decomp.nx] == decomp.rank
+        return recs[mine].copy(), np.nonzero(mine)[0].astype(np.int64)
+
+    def _halo(self):
+        d = self.d
+        if d.world == 1:
+            return np.zeros(0, PARTICLE_DTYPE), np.zeros(0, np.int64)
+        cols = cell_of(self.own, d.nx, d.ny) % d.nx
+        send = {}
+        for q in d.neighbours():
+            sel = np.isin(cols, d.send_cols(q))
+            send[q] = (self.own[sel], self.ranks[sel])
+        got = self.ex.exchange(send, d.neighbours())
+        recs = [got[q][0] for q in d.neighbours()]
+        rk = [got[q][1] for q in d.neighbours()]
+        return np.concatenate(recs) if recs else np.zeros(0, PARTICLE_DTYPE), \
+            np.concatenate(rk) if rk else np.zeros(0, np.int64)
+
+    def _migrate(self):
+        d = self.d
+        if d.world == 1:
+            return
+        dest = d.col_owner[cell_of(self.own, d.nx, d.ny) % d.nx]
+        stay = dest == d.rank
+        peers = d.neighbours()
+        if np.any(~stay & ~np.isin(dest, peers)):
+            raise RuntimeError("a particle moved more than one slab in one step")
+        send = {q: (self.own[dest == q], self.ranks[dest == q]) for q in peers}
+        got = self.ex.exchange(send, peers)
+        self.own = np.concatenate([self.own[stay]] + [got[q][0] for q in peers])
+        self.ranks = np.concatenate([self.ranks[stay]] + [got[q][1] for q in peers])
+
+    def _pair(self, kernel, par):
+        d = self.d
+        hrecs, hranks = self._halo()
+        n_own = len(self.own)
+        recs = np.concatenate([self.own, hrecs])
+        ranks = np.concatenate([self.ranks, hranks])
+        is_own = np.zeros(len(recs), bool)
+        is_own[:n_own] = True
+        c = cell_of(recs, d.nx, d.ny)
+        order = np.lexsort((ranks, c))
+        recs, ranks, is_own = recs[order], ranks[order], is_own[order]
+        self.be.pair(kernel, recs, ranks, d.nx, d.ny, d.owned_cells_mask(), par)
+        self.own, self.ranks = recs[is_own].copy(), ranks[is_own].copy()
+
+    def step(self, par: SphParams):
+        self.be.linear(KICK1, self.own, self.ranks, par)
+        self.be.linear(DRIFT, self.own, self.ranks, par)
+        self._migrate()
+        # build_grid writes p->cell for every particle (grid.cpp:156)
+        self.own["cell"] = cell_of(self.own, self.d.nx, self.d.ny)
+        self._pair(DENSITY, par)  # halo carries x, v_pred, m (and p, c from the last kick2)
+        self._pair(FORCE, par)    # fresh halo: rho updated by the owners' density
+        self.be.linear(KICK2, self.own, self.ranks, par)
+
+    def gather(self, group=None):
+        """All owned particles on every rank, in global ParticleStore::all order (tests)."""
+        import torch
+        import torch.distributed as dist
+        if self.d.world == 1:
+            order = np.argsort(self.ranks)
+            return self.own[order]
+        objs = [None] * self.d.world
+        dist.all_gather_object(objs, (self.own, self.ranks), group=group)
+        recs = np.concatenate([o[0] for o in objs])
+        ranks = np.concatenate([o[1] for o in objs])
+        return recs[np.argsort(ranks)]

@@ -169,6 +169,15 @@ class Context:
         _check(self.h, rc, "sph_bind")
         self.grid, self._ptrs, self._rank = grid, ptrs, rank
 
+    def set_owned_cells(self, mask: np.ndarray | None) -> None:
+        """Sweep only the cells with mask[c] != 0 (domain decomposition); None = all."""
+        self._need()
+        if mask is None:
+            _check(self.h, self.lib.sph_set_owned_cells(self.h, None), "sph_set_owned_cells")
+        else:
+            m = np.ascontiguousarray(mask, np.uint8)
+            _check(self.h, self.lib.sph_set_owned_cells(self.h, m.ctypes.data), "sph_set_owned_cells")
+
     def _need(self) -> None:
         if self.grid is None:
             raise _lib.SphError("context has no bound grid")

@@ -1,0 +1,149 @@
+"""Slab domain decomposition (paper_2502_16517_b200/decomp.py), world size 2 over gloo.
+
+The host-side logic (partition, migration, halo exchange, owned-cell sweeps) is checked
+on CPU with the oracle as the compute backend: k ranks must reproduce the single-rank
+reference step byte for byte. The GPU variant runs the same logic with the device backend
+(two processes sharing one GPU, gloo for the exchange).
+"""
+import os
+import socket
+import tempfile
+
+import numpy as np
+import pytest
+import torch.multiprocessing as mp
+
+from paper_2502_16517_b200.decomp import DistributedSim, Exchanger, SlabDecomposition, cell_of
+
+N, PPC, SEED, DT, STEPS = 6000, 64, 4, 1e-2, 3
+
+
+class OracleBackend:
+    """Test-only compute backend: the CPU oracle restatement."""
+
+    def __init__(self):
+        from oracle import Oracle
+        self.orc = Oracle()
+
+    def linear(self, kernel, recs, ranks, par):
+        n = len(recs)
+        self.orc.sweep(kernel, recs, 1, 1, 1.0, np.array([0, n], np.int64), np.arange(n, dtype=np.int64), par)
+
+    def pair(self, kernel, recs, ranks, nx, ny, mask, par):
+        c = cell_of(recs, nx, ny)
+        cb = np.zeros(nx * ny + 1, np.int64)
+        np.cumsum(np.bincount(c, minlength=nx * ny), out=cb[1:])
+        self.orc.sweep_masked(kernel, recs, nx, ny, 1.0 / nx, cb, np.arange(len(recs), dtype=np.int64),
+                              par, mask)
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def reference_run(orc, recs, par):
+    r = recs.copy()
+    nx = orc.grid_nx(len(r), PPC)
+    for _ in range(STEPS):
+        for k in (3, 2):
+            cb, li = orc.build_grid(r, nx)
+            orc.sweep(k, r, nx, nx, 1.0 / nx, cb, li, par)
+        cb, li = orc.build_grid(r, nx)
+        for k in (0, 1, 4):
+            orc.sweep(k, r, nx, nx, 1.0 / nx, cb, li, par)
+    return r
+
+
+def _worker(rank, world, port, out_path, use_gpu):
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    import torch.distributed as dist
+
+    from oracle import Oracle
+    from paper_2502_16517_b200 import Numerics, SphParams
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank,
+                            world_size=world)
+    orc = Oracle()
+    orc.threads = 2
+    recs, par = orc.make_particles(N, PPC, SEED)
+    par = SphParams(dt=DT, gamma=par.gamma, cfl=par.cfl, grav=par.grav,
+                    target_wcount=par.target_wcount)
+    nx = orc.grid_nx(N, PPC)
+    d = SlabDecomposition(nx, nx, world, rank)
+    own, ranks = DistributedSim.split_global(recs, d)
+    if use_gpu:
+        from paper_2502_16517_b200.decomp import DeviceBackend
+        be = DeviceBackend(0, numerics=Numerics.Exact)
+    else:
+        be = OracleBackend()
+        be.orc.threads = 2
+    sim = DistributedSim(d, own, ranks, be, Exchanger())
+    for _ in range(STEPS):
+        sim.step(par)
+    out = sim.gather()
+    if rank == 0:
+        np.save(out_path, out)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def _run(world, use_gpu):
+    port = _free_port()
+    with tempfile.TemporaryDirectory() as td:
+        out = os.path.join(td, "out.npy")
+        mp.spawn(_worker, args=(world, port, out, use_gpu), nprocs=world, join=True)
+        return np.load(out)
+
+
+def test_slab_geometry():
+    d = SlabDecomposition(17, 17, 3, 1)
+    assert list(d.owned_cols()) == list(range(5, 11))
+    assert list(d.halo_cols()) == [4, 11]
+    assert d.neighbours() == [0, 2]
+    assert list(d.send_cols(0)) == [5] and list(d.send_cols(2)) == [10]
+    d0 = SlabDecomposition(17, 17, 3, 0)
+    assert list(d0.halo_cols()) == [5, 16]  # torus wrap
+    m = d.owned_cells_mask()
+    assert m.sum() == 6 * 17 and m[5] and not m[4]
+    with pytest.raises(ValueError):
+        SlabDecomposition(5, 5, 3, 0)
+
+
+def test_split_partitions_every_particle(orc):
+    recs, _ = orc.make_particles(3000, 64, 2)
+    nx = orc.grid_nx(3000, 64)
+    seen = []
+    for r in range(3):
+        own, ranks = DistributedSim.split_global(recs, SlabDecomposition(nx, nx, 3, r))
+        seen.append(ranks)
+    allr = np.sort(np.concatenate(seen))
+    assert np.array_equal(allr, np.arange(3000))
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_decomposed_steps_equal_single_rank(orc, world):
+    """world ranks (gloo, oracle compute) == the single-rank reference, byte for byte."""
+    from paper_2502_16517_b200 import SphParams
+    recs, par = orc.make_particles(N, PPC, SEED)
+    par = SphParams(dt=DT, gamma=par.gamma, cfl=par.cfl, grav=par.grav,
+                    target_wcount=par.target_wcount)
+    ref = reference_run(orc, recs, par)
+    assert np.count_nonzero(ref["cell"] != recs["cell"]) > 0  # particles changed cells
+    got = _run(world, use_gpu=False)
+    assert got.tobytes() == ref.tobytes()
+
+
+@pytest.mark.gpu
+def test_decomposed_steps_on_device_equal_single_rank(orc):
+    """Same, with the device backend (EXACT) for both ranks on one GPU."""
+    from paper_2502_16517_b200 import SphParams
+    recs, par = orc.make_particles(N, PPC, SEED)
+    par = SphParams(dt=DT, gamma=par.gamma, cfl=par.cfl, grav=par.grav,
+                    target_wcount=par.target_wcount)
+    ref = reference_run(orc, recs, par)
+    got = _run(2, use_gpu=True)
+    assert got.tobytes() == ref.tobytes()
