@@ -445,6 +445,13 @@ struct sph_ctx {
     A.grav = par.grav;
     A.aos = aos.p;
     A.soa = soa;
+    if (!exact && cull) { // spatial j order + far-chunk gravity-only path
+      boxes.ensure((size_t)n / 32 + (size_t)ncells + 2);
+      launch_chunk_boxes(boxes.p, ilist.p, aos.p, soa, use_aos, cell_begin.p, ncells, stream);
+      launched();
+      A.boxes = boxes.p;
+      A.jlist = ilist.p;
+    }
     if (exact) launch_force_exact(A, n_items0, use_aos, stream);
     else launch_force_fast(A, n_items0, use_aos, stream);
     launched();

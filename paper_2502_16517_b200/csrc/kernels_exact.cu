@@ -216,6 +216,10 @@ struct ExactPolicy {
     s.hdt -= pv.y * dvdr * inv_r * dwi * 0.5 * I.hi;
   }
 
+  __device__ static void for_tile_far(const FI &I, const ForTile &T, FA &s) {
+    for_tile<true>(I, T, s); // never used: EXACT walks every chunk as near
+  }
+
   template <bool MINIMG>
   __device__ static void for_tile(const FI &I, const ForTile &T, FA &s) {
 #pragma unroll 2

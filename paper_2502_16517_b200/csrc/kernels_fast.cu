@@ -286,6 +286,18 @@ struct FastPolicy {
     }
   }
 
+  // Gravity only (chunk out of every lane's support): branch-free, shifted images.
+  __device__ static void for_tile_far(const FI &I, const ForTile &T, FA &s) {
+#pragma unroll 4
+    for (int j = 0; j < kTJ; ++j) {
+      const double2 xj = T.xy[j];
+      const double dx = I.x - xj.x, dy = I.y - xj.y;
+      const double f = T.mg[j].y * rsqrt3_fast(fma(dx, dx, fma(dy, dy, I.eps2)));
+      s.ax = fma(-f, dx, s.ax);
+      s.ay = fma(-f, dy, s.ay);
+    }
+  }
+
   __device__ static void for_publish(const FI &I, const FA &s, double o[5]) {
     o[0] = s.ax;
     o[1] = s.ay;

@@ -266,7 +266,7 @@ __global__ void __launch_bounds__(1024) make_items_kernel(Item *__restrict__ ite
                                                           const int *__restrict__ cell_begin,
                                                           const int *__restrict__ na_cell,
                                                           const int *__restrict__ order,
-                                                          int ncells) {
+                                                          int ncells, int tile) {
   typedef cub::BlockScan<int, 1024> Scan;
   typedef cub::BlockReduce<long long, 1024> Red;
   __shared__ typename Scan::TempStorage ts;
@@ -280,7 +280,7 @@ __global__ void __launch_bounds__(1024) make_items_kernel(Item *__restrict__ ite
     const int c = (ci < ncells && order) ? order[ci] : ci;
     int k = 0;
     if (ci < ncells) {
-      k = (cnt[c] + kTI - 1) / kTI;
+      k = (cnt[c] + tile - 1) / tile;
       pairs += (long long)cnt[c] * na_cell[c];
     }
     int off, tot;
@@ -290,8 +290,8 @@ __global__ void __launch_bounds__(1024) make_items_kernel(Item *__restrict__ ite
       for (int q = 0; q < k; ++q) {
         Item it;
         it.cell = c;
-        it.start = cell_begin[c] + q * kTI;
-        it.count = min(kTI, cnt[c] - q * kTI);
+        it.start = cell_begin[c] + q * tile;
+        it.count = min(tile, cnt[c] - q * tile);
         it.pad = 0;
         items[base + off + q] = it;
       }
@@ -420,9 +420,9 @@ void launch_spatial_order(int *ilist, const Particle *aos, const SoaMirror &f, b
 }
 void launch_make_items(Item *items, int *n_items_out, long long *pairs_out, const int *cnt,
                        const int *cell_begin, const int *na_cell, const int *order, int ncells,
-                       cudaStream_t s) {
+                       cudaStream_t s, int tile) {
   make_items_kernel<<<1, 1024, 0, s>>>(items, n_items_out, pairs_out, cnt, cell_begin, na_cell,
-                                       order, ncells);
+                                       order, ncells, tile);
 }
 void launch_chunk_boxes(float4 *boxes, const int *ilist, const Particle *aos, const SoaMirror &f,
                         bool aos_src, const int *cell_begin, int ncells, cudaStream_t s) {

@@ -71,6 +71,8 @@ struct ForArgs {
   double grav;
   const Particle *aos;
   SoaMirror soa;
+  const int *jlist;     // FAST: j in spatial order (ilist); null = reference order
+  const float4 *boxes;  // FAST: chunk boxes -> far chunks take the gravity-only path
 };
 
 // ---- j staging (gather one active record into the SoA tile) ----
@@ -110,6 +112,7 @@ struct ActiveLayout {
   int cell[9];    // stencil cell ids
   int na;         // active particles
   int pre[10];    // prefix of counts
+  int nch[10];    // prefix of 32-chunks per stencil cell
   int base[9];    // first slot of each stencil cell
   double sx[9], sy[9]; // periodic image shift of each stencil cell
 };
@@ -127,6 +130,8 @@ __device__ __forceinline__ void build_active(const Geom &g, int c, ActiveLayout 
     L.sy[k] = st.sy[k];
   }
   L.na = L.pre[st.n];
+  L.nch[0] = 0;
+  for (int k = 0; k < st.n; ++k) L.nch[k + 1] = L.nch[k] + (L.pre[k + 1] - L.pre[k] + 31) / 32;
 }
 
 // Active position p -> (slot, stencil index).
@@ -242,8 +247,81 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, SPH_MINB_DEN) density_round
   }
 }
 
+__device__ __forceinline__ int chunk_box_index(int cell_begin_c, int c, int k) {
+  return (cell_begin_c >> 5) + c + k;
+}
+
+__device__ __forceinline__ float warp_min(float v) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) v = fminf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+__device__ __forceinline__ float warp_max(float v) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+// Chunk g of the active list -> (stencil cell nb, chunk k within it).
+__device__ __forceinline__ void chunk_locate(const ActiveLayout &L, int g, int &nb, int &k) {
+  nb = 0;
+#pragma unroll 1
+  while (nb + 1 < L.n && g >= L.nch[nb + 1]) ++nb;
+  k = g - L.nch[nb];
+}
+
+// Warp box (or a single point) against the FP32 box of chunk (nb, k), shifted to the
+// periodic image of stencil cell nb: true if some pair can be within `reach`.
+__device__ __forceinline__ bool chunk_near(const ActiveLayout &L, const float4 *boxes, int nb, int k,
+                                           float xlo, float xhi, float ylo, float yhi,
+                                           float reach2) {
+  const float4 b = boxes[chunk_box_index(L.base[nb], L.cell[nb], k)];
+  const float sx = (float)L.sx[nb], sy = (float)L.sy[nb];
+  const float gx = fmaxf(0.0f, fmaxf(b.x + sx - xhi, xlo - (b.z + sx)));
+  const float gy = fmaxf(0.0f, fmaxf(b.y + sy - yhi, ylo - (b.w + sy)));
+  return gx * gx + gy * gy <= reach2;
+}
+
+// Visits the chunks of the active list in order, 32 at a time: lane l evaluates chunk
+// g0 + l (box test, all lanes in parallel), a ballot gives the batch's chunk set, and the
+// chunks are handed to `visit(nb, k, near, next_nb, next_k, has_next)` in order so the
+// caller can prefetch the next chunk. ALL_CHUNKS: every chunk is visited (near = box test);
+// otherwise only near chunks are.
+template <bool ALL_CHUNKS, class Visit>
+__device__ __forceinline__ void walk_chunks(const ActiveLayout &L, const float4 *boxes, bool test,
+                                            float xlo, float xhi, float ylo, float yhi,
+                                            float reach2, Visit &&visit) {
+  const int lane = threadIdx.x & 31;
+  const int total = L.nch[L.n];
+  for (int g0 = 0; g0 < total; g0 += 32) {
+    const int g = g0 + lane;
+    int nb = 0, k = 0;
+    bool valid = g < total, near = valid;
+    if (valid) {
+      chunk_locate(L, g, nb, k);
+      if (test) near = chunk_near(L, boxes, nb, k, xlo, xhi, ylo, yhi, reach2);
+    }
+    const unsigned vmask = __ballot_sync(0xffffffffu, valid);
+    const unsigned nmask = __ballot_sync(0xffffffffu, near);
+    unsigned todo = ALL_CHUNKS ? vmask : nmask;
+    while (todo) {
+      const int b = __ffs(todo) - 1;
+      todo &= todo - 1;
+      const int bn = todo ? __ffs(todo) - 1 : 0;
+      const int cnb = __shfl_sync(0xffffffffu, nb, b), ck = __shfl_sync(0xffffffffu, k, b);
+      const int nnb = __shfl_sync(0xffffffffu, nb, bn), nk = __shfl_sync(0xffffffffu, k, bn);
+      visit(cnb, ck, ((nmask >> b) & 1u) != 0u, nnb, nk, todo != 0u);
+    }
+  }
+}
+
 // ---------------------------------------------------------------------------------------
-// Force sweep.
+// Force sweep. The active list is walked per stencil cell in 32-particle chunks (chunk
+// prefix kept in shared memory, so no per-lane search); the next chunk's loads are in
+// flight while the current one is consumed. With FAST numerics the chunks follow the
+// spatial ilist order and a chunk farther than the warp's support reach from the warp's
+// bounding box takes the gravity-only path (the softened gravity acts on every active
+// pair, kernels.cpp:128-131, but no SPH term can be in support there).
 // ---------------------------------------------------------------------------------------
 template <class P, bool AOS>
 __global__ void __launch_bounds__(kWarpsPerCta * 32, SPH_MINB_FOR) force_kernel(ForArgs A) {
@@ -260,21 +338,32 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, SPH_MINB_FOR) force_kernel(
   if constexpr (AOS) src.p = A.aos; else src.f = A.soa;
   const bool live = lane < it.count;
   const int slot = A.list[it.start + (live ? lane : 0)];
-  typename P::FI I = P::for_i(src.x(slot), src.vp(slot), src.h(slot), src.pr(slot),
-                              src.rho(slot), src.rho_dh(slot), src.c(slot), src.div_v(slot),
-                              src.rot_v(slot), A.grav);
+  const double2 xi = src.x(slot);
+  const double hi = src.h(slot);
+  typename P::FI I = P::for_i(xi, src.vp(slot), hi, src.pr(slot), src.rho(slot),
+                              src.rho_dh(slot), src.c(slot), src.div_v(slot), src.rot_v(slot),
+                              A.grav);
   typename P::FA s = P::for_zero(src.h_dt(slot));
+  const bool cull = A.boxes != nullptr;
+  float ixlo = 0.f, ixhi = 0.f, iylo = 0.f, iyhi = 0.f, reach2 = 0.f;
+  if (cull) {
+    ixlo = warp_min((float)xi.x);
+    ixhi = warp_max((float)xi.x);
+    iylo = warp_min((float)xi.y);
+    iyhi = warp_max((float)xi.y);
+    const float reach = warp_max((float)(2.5 * hi)) * (1.0f + 1e-5f) + 1e-6f;
+    reach2 = reach * reach;
+  }
   __syncwarp();
   const bool minimg = P::kExactOrder || !A.g.use_shift;
-  const int na = L.na, ntiles = (na + kTJ - 1) / kTJ;
 
   double2 rx, rv;
   double rm, rrho, rp, rc;
-  auto gather = [&](int k) {
-    const int p = k * kTJ + lane;
-    if (p < na) {
-      int nb;
-      const int sj = active_slot(L, p, nb);
+  auto gather = [&](int nb, int k) {
+    const int cnt = L.pre[nb + 1] - L.pre[nb];
+    const int q = k * kTJ + lane;
+    if (q < cnt) {
+      const int sj = A.jlist ? A.jlist[L.base[nb] + q] : L.base[nb] + q;
       rx = src.x(sj);
       rv = src.vp(sj);
       rm = src.m(sj);
@@ -288,8 +377,10 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, SPH_MINB_FOR) force_kernel(
       rm = 0.0; rrho = 1.0; rp = 0.0; rc = 0.0;
     }
   };
-  if (ntiles > 0) gather(0);
-  for (int k = 0; k < ntiles; ++k) {
+  bool staged = false; // registers already hold the chunk about to be consumed
+  walk_chunks<true>(L, A.boxes, cull && !minimg, ixlo, ixhi, iylo, iyhi, reach2,
+                    [&](int nb, int k, bool near, int nnb, int nk, bool has_next) {
+    if (!staged) gather(nb, k);
     T.xy[lane] = rx;
     T.vv[lane] = rv;
     const double4 d = P::stage_force(rm, rrho, rp, A.grav); // (m, gm, pv.x, pv.y)
@@ -297,11 +388,13 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, SPH_MINB_FOR) force_kernel(
     T.pv[lane] = make_double2(d.z, d.w);
     T.c[lane] = rc;
     __syncwarp();
-    if (k + 1 < ntiles) gather(k + 1);
+    staged = has_next;
+    if (has_next) gather(nnb, nk); // loads in flight during this chunk
     if (minimg) P::template for_tile<true>(I, T, s);
-    else P::template for_tile<false>(I, T, s);
+    else if (near) P::template for_tile<false>(I, T, s);
+    else P::template for_tile_far(I, T, s);
     __syncwarp();
-  }
+  });
   if (!live) return;
   double o[5]; // a0, a1, u_dt, v_sig, h_dt
   P::for_publish(I, s, o);
@@ -323,21 +416,6 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, SPH_MINB_FOR) force_kernel(
 // without being loaded. Boxes are in FP32 with an absolute safety margin of 1e-6.
 // Chunk k of cell c has box index (cell_begin[c] >> 5) + c + k (unique, no scan needed).
 // ---------------------------------------------------------------------------------------
-__device__ __forceinline__ int chunk_box_index(int cell_begin_c, int c, int k) {
-  return (cell_begin_c >> 5) + c + k;
-}
-
-__device__ __forceinline__ float warp_min(float v) {
-#pragma unroll
-  for (int o = 16; o; o >>= 1) v = fminf(v, __shfl_xor_sync(0xffffffffu, v, o));
-  return v;
-}
-__device__ __forceinline__ float warp_max(float v) {
-#pragma unroll
-  for (int o = 16; o; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
-  return v;
-}
-
 template <class P, bool AOS>
 __global__ void __launch_bounds__(kWarpsPerCta * 32, SPH_MINB_DEN) density_cull_kernel(DenArgs A) {
   __shared__ DenTile tiles[kWarpsPerCta];
@@ -365,36 +443,37 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, SPH_MINB_DEN) density_cull_
   const float reach2 = reach * reach;
   __syncwarp();
   const bool minimg = !A.g.use_shift;
-  for (int nb = 0; nb < L.n; ++nb) {
-    const int base = L.base[nb], cnt = L.pre[nb + 1] - L.pre[nb];
-    const float sx = (float)L.sx[nb], sy = (float)L.sy[nb];
-    const float4 *bx = A.boxes + chunk_box_index(base, L.cell[nb], 0);
-    for (int k = 0; k * kTJ < cnt; ++k) {
-      if (!minimg) {
-        const float4 b = bx[k]; // (xlo, ylo, xhi, yhi), same address for all lanes
-        const float gx = fmaxf(0.0f, fmaxf(b.x + sx - ixhi, ixlo - (b.z + sx)));
-        const float gy = fmaxf(0.0f, fmaxf(b.y + sy - iyhi, iylo - (b.w + sy)));
-        if (gx * gx + gy * gy > reach2) continue; // warp-uniform
-      }
-      const int q = k * kTJ + lane;
-      if (q < cnt) {
-        const int sj = A.jlist[base + q];
-        double2 rx = src.x(sj);
-        if (!minimg) { rx.x += L.sx[nb]; rx.y += L.sy[nb]; }
-        T.xy[lane] = rx;
-        T.vv[lane] = src.vp(sj);
-        T.m[lane] = src.m(sj);
-      } else {
-        T.xy[lane] = make_double2(kDummyX, kDummyX);
-        T.vv[lane] = make_double2(0.0, 0.0);
-        T.m[lane] = 0.0;
-      }
-      __syncwarp();
-      if (minimg) P::template den_tile<true>(I, T, s);
-      else P::template den_tile<false>(I, T, s);
-      __syncwarp();
+  double2 rx, rv;
+  double rm;
+  auto gather = [&](int nb, int k) {
+    const int cnt = L.pre[nb + 1] - L.pre[nb];
+    const int q = k * kTJ + lane;
+    if (q < cnt) {
+      const int sj = A.jlist[L.base[nb] + q];
+      rx = src.x(sj);
+      if (!minimg) { rx.x += L.sx[nb]; rx.y += L.sy[nb]; }
+      rv = src.vp(sj);
+      rm = src.m(sj);
+    } else {
+      rx = make_double2(kDummyX, kDummyX);
+      rv = make_double2(0.0, 0.0);
+      rm = 0.0;
     }
-  }
+  };
+  bool staged = false;
+  walk_chunks<false>(L, A.boxes, !minimg, ixlo, ixhi, iylo, iyhi, reach2,
+                     [&](int nb, int k, bool, int nnb, int nk, bool has_next) {
+    if (!staged) gather(nb, k);
+    T.xy[lane] = rx;
+    T.vv[lane] = rv;
+    T.m[lane] = rm;
+    __syncwarp();
+    staged = has_next;
+    if (has_next) gather(nnb, nk);
+    if (minimg) P::template den_tile<true>(I, T, s);
+    else P::template den_tile<false>(I, T, s);
+    __syncwarp();
+  });
   if (!live) return;
   double hn = h;
   const int st = P::den_step(s, hn, A.target, A.h_max, A.round);

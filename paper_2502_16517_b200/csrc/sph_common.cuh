@@ -43,7 +43,8 @@ enum Field : uint32_t {
 
 // Access sets per kernel (reference view descriptors kernels.cpp:741-859).
 // IN = fields read, OUT = fields written.
-constexpr uint32_t DEN_IN = F_X | F_VPRED | F_M | F_H;
+// flags is read-modify-write on a failed h-iteration (kernels.cpp:222), so it is InOut
+constexpr uint32_t DEN_IN = F_X | F_VPRED | F_M | F_H | F_FLAGS;
 constexpr uint32_t DEN_OUT = F_H | F_RHO | F_WCOUNT | F_RHODH | F_ROTV | F_DIVV | F_FLAGS;
 constexpr uint32_t FOR_IN = F_X | F_VPRED | F_M | F_H | F_P | F_RHO | F_RHODH | F_C | F_DIVV |
                             F_ROTV | F_HDT;

@@ -41,7 +41,7 @@ void launch_spatial_order(int *ilist, const Particle *aos, const SoaMirror &f, b
 // Items are emitted in `order` (cells sorted by descending cost bucket; may be null).
 void launch_make_items(Item *items, int *n_items_out, long long *pairs_out, const int *cnt,
                        const int *cell_begin, const int *na_cell, const int *order, int ncells,
-                       cudaStream_t s);
+                       cudaStream_t s, int tile = 32);
 // FP32 bounding boxes of the 32-chunks of each cell's ilist (culled FAST density)
 void launch_chunk_boxes(float4 *boxes, const int *ilist, const Particle *aos, const SoaMirror &f,
                         bool aos_src, const int *cell_begin, int ncells, cudaStream_t s);
