@@ -210,6 +210,8 @@ struct sph_ctx {
   DevBuf<double> hcur, wc;
   DevBuf<unsigned char> rounds, again;
   DevBuf<float4> boxes;
+  DevBuf<double2> jv_xy, jv_vv, jv_mg, jv_pv;
+  DevBuf<double> jv_m, jv_c;
   bool cull = true; // FAST density: spatial j order + chunk culling (env SPH_B200_CULL=0 disables)
   DevBuf<char> dense, cub_tmp;
   PinnedBuf h_stage, h_small;
@@ -247,6 +249,7 @@ struct sph_ctx {
     cell_order.release(); cell_order_in.release(); items0.release(); items_a.release();
     items_b.release(); hcur.release(); wc.release(); rounds.release(); dense.release();
     cub_tmp.release(); h_stage.release(); h_small.release(); owned.release();
+    jv_xy.release(); jv_vv.release(); jv_mg.release(); jv_pv.release(); jv_m.release(); jv_c.release();
   }
 
   Geom geom() const {
@@ -377,9 +380,14 @@ struct sph_ctx {
     if (!exact && !meanw && cull) {
       boxes.ensure((size_t)n / 32 + (size_t)ncells + 2);
       launch_chunk_boxes(boxes.p, ilist.p, aos.p, soa, use_aos, cell_begin.p, ncells, stream);
-      launched();
+      jv_xy.ensure(n); jv_vv.ensure(n); jv_m.ensure(n);
+      launch_jview_density(jv_xy.p, jv_vv.p, jv_m.p, ilist.p, aos.p, soa, use_aos, (int)n, stream);
+      launched(2);
       A.boxes = boxes.p;
       A.jlist = ilist.p;
+      A.jv.xy = jv_xy.p;
+      A.jv.vv = jv_vv.p;
+      A.jv.m = jv_m.p;
     }
     const Item *items = items0.p;
     const int *list = ilist.p;
@@ -448,9 +456,17 @@ struct sph_ctx {
     if (!exact && cull) { // spatial j order + far-chunk gravity-only path
       boxes.ensure((size_t)n / 32 + (size_t)ncells + 2);
       launch_chunk_boxes(boxes.p, ilist.p, aos.p, soa, use_aos, cell_begin.p, ncells, stream);
-      launched();
+      jv_xy.ensure(n); jv_vv.ensure(n); jv_mg.ensure(n); jv_pv.ensure(n); jv_c.ensure(n);
+      launch_jview_force(jv_xy.p, jv_vv.p, jv_mg.p, jv_pv.p, jv_c.p, ilist.p, aos.p, soa, use_aos,
+                         (int)n, par.grav, stream);
+      launched(2);
       A.boxes = boxes.p;
       A.jlist = ilist.p;
+      A.jv.xy = jv_xy.p;
+      A.jv.vv = jv_vv.p;
+      A.jv.mg = jv_mg.p;
+      A.jv.pv = jv_pv.p;
+      A.jv.c = jv_c.p;
     }
     if (exact) launch_force_exact(A, n_items0, use_aos, stream);
     else launch_force_fast(A, n_items0, use_aos, stream);

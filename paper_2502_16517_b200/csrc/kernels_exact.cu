@@ -368,8 +368,8 @@ void launch_force_exact(const ForArgs &a, int n_items, bool aos, cudaStream_t s)
   ForArgs b = a;
   b.n_items = n_items;
   const int G = pair_grid(n_items), B = kWarpsPerCta * 32;
-  if (aos) force_kernel<ExactPolicy, true><<<G, B, 0, s>>>(b);
-  else force_kernel<ExactPolicy, false><<<G, B, 0, s>>>(b);
+  if (aos) force_kernel<ExactPolicy, true, false><<<G, B, 0, s>>>(b);
+  else force_kernel<ExactPolicy, false, false><<<G, B, 0, s>>>(b);
 }
 
 void launch_linear(int kernel, bool aos, Particle *p, const SoaMirror &f, int n, const Params &par,

@@ -307,6 +307,55 @@ struct FastPolicy {
   }
 };
 
+// j-view builders: gather the sweep's j fields into ilist order (+ hoisted invariants).
+template <bool AOS>
+__global__ void jview_density_kernel(double2 *xy, double2 *vv, double *m, const int *ilist,
+                                     const Particle *aos, SoaMirror f, int n) {
+  const int p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= n) return;
+  JSrc<AOS> src;
+  if constexpr (AOS) src.p = aos; else src.f = f;
+  const int sj = ilist[p];
+  xy[p] = src.x(sj);
+  vv[p] = src.vp(sj);
+  m[p] = src.m(sj);
+}
+
+template <bool AOS>
+__global__ void jview_force_kernel(double2 *xy, double2 *vv, double2 *mg, double2 *pv, double *c,
+                                   const int *ilist, const Particle *aos, SoaMirror f, int n,
+                                   double grav) {
+  const int p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= n) return;
+  JSrc<AOS> src;
+  if constexpr (AOS) src.p = aos; else src.f = f;
+  const int sj = ilist[p];
+  xy[p] = src.x(sj);
+  vv[p] = src.vp(sj);
+  const double4 d = FastPolicy::stage_force(src.m(sj), src.rho(sj), src.pr(sj), grav);
+  mg[p] = make_double2(d.x, d.y);
+  pv[p] = make_double2(d.z, d.w);
+  c[p] = src.c(sj);
+}
+
+void launch_jview_density(double2 *xy, double2 *vv, double *m, const int *ilist,
+                          const Particle *aos, const SoaMirror &f, bool use_aos, int n,
+                          cudaStream_t s) {
+  if (n <= 0) return;
+  if (use_aos) jview_density_kernel<true><<<(n + 255) / 256, 256, 0, s>>>(xy, vv, m, ilist, aos, f, n);
+  else jview_density_kernel<false><<<(n + 255) / 256, 256, 0, s>>>(xy, vv, m, ilist, aos, f, n);
+}
+
+void launch_jview_force(double2 *xy, double2 *vv, double2 *mg, double2 *pv, double *c,
+                        const int *ilist, const Particle *aos, const SoaMirror &f, bool use_aos,
+                        int n, double grav, cudaStream_t s) {
+  if (n <= 0) return;
+  if (use_aos)
+    jview_force_kernel<true><<<(n + 255) / 256, 256, 0, s>>>(xy, vv, mg, pv, c, ilist, aos, f, n, grav);
+  else
+    jview_force_kernel<false><<<(n + 255) / 256, 256, 0, s>>>(xy, vv, mg, pv, c, ilist, aos, f, n, grav);
+}
+
 void launch_density_fast(const DenArgs &a, int n_items, bool aos, cudaStream_t s) {
   if (n_items <= 0) return;
   DenArgs b = a;
@@ -326,8 +375,13 @@ void launch_force_fast(const ForArgs &a, int n_items, bool aos, cudaStream_t s) 
   ForArgs b = a;
   b.n_items = n_items;
   const int G = pair_grid(n_items), B = kWarpsPerCta * 32;
-  if (aos) force_kernel<FastPolicy, true><<<G, B, 0, s>>>(b);
-  else force_kernel<FastPolicy, false><<<G, B, 0, s>>>(b);
+  if (b.jv.xy) {
+    if (aos) force_kernel<FastPolicy, true, true><<<G, B, 0, s>>>(b);
+    else force_kernel<FastPolicy, false, true><<<G, B, 0, s>>>(b);
+  } else {
+    if (aos) force_kernel<FastPolicy, true, false><<<G, B, 0, s>>>(b);
+    else force_kernel<FastPolicy, false, false><<<G, B, 0, s>>>(b);
+  }
 }
 
 } // namespace sphb

@@ -46,6 +46,18 @@ constexpr double kDummyX = 1.0e30;
 #define SPH_MINB_FOR 5
 #endif
 
+// Per-sweep j-view (FAST numerics): the fields a pair sweep reads from its active
+// particles, gathered once per sweep into SoA arrays in the spatial ilist order (index =
+// cell_begin[c] + position in the cell's ilist), with the per-j invariants hoisted
+// (grav*m, m*p/rho^2, m/rho). Chunk gathers are then contiguous loads with no
+// indirection and no division — the paper's AoS->SoA view, built once instead of per tile.
+struct JView {
+  const double2 *xy, *vv; // position, v_pred
+  const double *m;        // density: m
+  const double2 *mg, *pv; // force: (m, grav*m), (m*p/rho^2, m/rho)
+  const double *c;        // force: sound speed
+};
+
 struct DenArgs {
   Geom g;
   const Item *items;
@@ -61,6 +73,7 @@ struct DenArgs {
   double *wc_out;       // mean_wcount mode: per-slot neighbour sum (grid.cpp:36-50)
   const int *jlist;     // culled FAST sweep: cell-major slots in spatial order (ilist)
   const float4 *boxes;  // culled FAST sweep: bounding box of each 32-chunk of jlist
+  JView jv;             // culled FAST sweep: j-view in jlist order
 };
 
 struct ForArgs {
@@ -73,6 +86,7 @@ struct ForArgs {
   SoaMirror soa;
   const int *jlist;     // FAST: j in spatial order (ilist); null = reference order
   const float4 *boxes;  // FAST: chunk boxes -> far chunks take the gravity-only path
+  JView jv;             // FAST: j-view in jlist order (null xy = gather from the mirror)
 };
 
 // ---- j staging (gather one active record into the SoA tile) ----
@@ -323,7 +337,7 @@ __device__ __forceinline__ void walk_chunks(const ActiveLayout &L, const float4 
 // bounding box takes the gravity-only path (the softened gravity acts on every active
 // pair, kernels.cpp:128-131, but no SPH term can be in support there).
 // ---------------------------------------------------------------------------------------
-template <class P, bool AOS>
+template <class P, bool AOS, bool VIEW>
 __global__ void __launch_bounds__(kWarpsPerCta * 32, SPH_MINB_FOR) force_kernel(ForArgs A) {
   __shared__ ForTile tiles[kWarpsPerCta];
   __shared__ ActiveLayout lay[kWarpsPerCta];
@@ -357,39 +371,58 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, SPH_MINB_FOR) force_kernel(
   __syncwarp();
   const bool minimg = P::kExactOrder || !A.g.use_shift;
 
-  double2 rx, rv;
+  double2 rx, rv, rmg, rpv;
   double rm, rrho, rp, rc;
+  constexpr bool view = VIEW;
   auto gather = [&](int nb, int k) {
     const int cnt = L.pre[nb + 1] - L.pre[nb];
     const int q = k * kTJ + lane;
     if (q < cnt) {
-      const int sj = A.jlist ? A.jlist[L.base[nb] + q] : L.base[nb] + q;
-      rx = src.x(sj);
-      rv = src.vp(sj);
-      rm = src.m(sj);
-      rrho = src.rho(sj);
-      rp = src.pr(sj);
-      rc = src.c(sj);
-      if (!minimg) { rx.x += L.sx[nb]; rx.y += L.sy[nb]; }
+      const int idx = L.base[nb] + q;
+      if constexpr (VIEW) { // contiguous j-view loads, derived terms precomputed
+        rx = A.jv.xy[idx];
+        rv = A.jv.vv[idx];
+        rmg = A.jv.mg[idx];
+        rpv = A.jv.pv[idx];
+        rc = A.jv.c[idx];
+      } else {
+        const int sj = A.jlist ? A.jlist[idx] : idx;
+        rx = src.x(sj);
+        rv = src.vp(sj);
+        rm = src.m(sj);
+        rrho = src.rho(sj);
+        rp = src.pr(sj);
+        rc = src.c(sj);
+      }
     } else { // inert padding: r2 <= 0 (exact) or gm = 0 (fast)
       rx = make_double2(kDummyX, kDummyX);
       rv = make_double2(0.0, 0.0);
       rm = 0.0; rrho = 1.0; rp = 0.0; rc = 0.0;
+      rmg = make_double2(0.0, 0.0);
+      rpv = make_double2(0.0, 0.0);
     }
   };
   bool staged = false; // registers already hold the chunk about to be consumed
+  int gnb = 0;          // stencil cell of the staged chunk (periodic shift applied at staging)
   walk_chunks<true>(L, A.boxes, cull && !minimg, ixlo, ixhi, iylo, iyhi, reach2,
                     [&](int nb, int k, bool near, int nnb, int nk, bool has_next) {
-    if (!staged) gather(nb, k);
-    T.xy[lane] = rx;
+    if (!staged) { gather(nb, k); gnb = nb; }
+    double2 sxy = rx;
+    if (!minimg) { sxy.x += L.sx[gnb]; sxy.y += L.sy[gnb]; }
+    T.xy[lane] = sxy;
     T.vv[lane] = rv;
-    const double4 d = P::stage_force(rm, rrho, rp, A.grav); // (m, gm, pv.x, pv.y)
-    T.mg[lane] = make_double2(d.x, d.y);
-    T.pv[lane] = make_double2(d.z, d.w);
+    if constexpr (VIEW) {
+      T.mg[lane] = rmg;
+      T.pv[lane] = rpv;
+    } else {
+      const double4 d = P::stage_force(rm, rrho, rp, A.grav); // (m, gm, pv.x, pv.y)
+      T.mg[lane] = make_double2(d.x, d.y);
+      T.pv[lane] = make_double2(d.z, d.w);
+    }
     T.c[lane] = rc;
     __syncwarp();
     staged = has_next;
-    if (has_next) gather(nnb, nk); // loads in flight during this chunk
+    if (has_next) { gather(nnb, nk); gnb = nnb; } // loads in flight during this chunk
     if (minimg) P::template for_tile<true>(I, T, s);
     else if (near) P::template for_tile<false>(I, T, s);
     else P::template for_tile_far(I, T, s);
@@ -449,11 +482,17 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, SPH_MINB_DEN) density_cull_
     const int cnt = L.pre[nb + 1] - L.pre[nb];
     const int q = k * kTJ + lane;
     if (q < cnt) {
-      const int sj = A.jlist[L.base[nb] + q];
-      rx = src.x(sj);
-      if (!minimg) { rx.x += L.sx[nb]; rx.y += L.sy[nb]; }
-      rv = src.vp(sj);
-      rm = src.m(sj);
+      const int idx = L.base[nb] + q;
+      if (A.jv.xy) {
+        rx = A.jv.xy[idx];
+        rv = A.jv.vv[idx];
+        rm = A.jv.m[idx];
+      } else {
+        const int sj = A.jlist[idx];
+        rx = src.x(sj);
+        rv = src.vp(sj);
+        rm = src.m(sj);
+      }
     } else {
       rx = make_double2(kDummyX, kDummyX);
       rv = make_double2(0.0, 0.0);
@@ -461,15 +500,18 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, SPH_MINB_DEN) density_cull_
     }
   };
   bool staged = false;
+  int gnb = 0;
   walk_chunks<false>(L, A.boxes, !minimg, ixlo, ixhi, iylo, iyhi, reach2,
                      [&](int nb, int k, bool, int nnb, int nk, bool has_next) {
-    if (!staged) gather(nb, k);
-    T.xy[lane] = rx;
+    if (!staged) { gather(nb, k); gnb = nb; }
+    double2 sxy = rx;
+    if (!minimg) { sxy.x += L.sx[gnb]; sxy.y += L.sy[gnb]; }
+    T.xy[lane] = sxy;
     T.vv[lane] = rv;
     T.m[lane] = rm;
     __syncwarp();
     staged = has_next;
-    if (has_next) gather(nnb, nk);
+    if (has_next) { gather(nnb, nk); gnb = nnb; }
     if (minimg) P::template den_tile<true>(I, T, s);
     else P::template den_tile<false>(I, T, s);
     __syncwarp();

@@ -13,6 +13,14 @@ void launch_force_exact(const ForArgs &a, int n_items, bool aos, cudaStream_t s)
 void launch_density_fast(const DenArgs &a, int n_items, bool aos, cudaStream_t s);
 void launch_force_fast(const ForArgs &a, int n_items, bool aos, cudaStream_t s);
 
+// FAST j-views (kernels_fast.cu): sweep j fields in ilist order with hoisted invariants
+void launch_jview_density(double2 *xy, double2 *vv, double *m, const int *ilist,
+                          const Particle *aos, const SoaMirror &f, bool use_aos, int n,
+                          cudaStream_t s);
+void launch_jview_force(double2 *xy, double2 *vv, double2 *mg, double2 *pv, double *c,
+                        const int *ilist, const Particle *aos, const SoaMirror &f, bool use_aos,
+                        int n, double grav, cudaStream_t s);
+
 // streaming kernels (kernels_exact.cu); kernel = SPH_DRIFT / SPH_KICK1 / SPH_KICK2
 void launch_linear(int kernel, bool aos, Particle *p, const SoaMirror &f, int n, const Params &par,
                    cudaStream_t s);
