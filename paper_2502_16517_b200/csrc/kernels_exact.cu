@@ -156,12 +156,14 @@ struct ExactPolicy {
     o[5] = s.div_v * inv_h3;
   }
 
+  struct FCold { double pad; };
   struct FI { double x0, x1, v0, v1, hi, inv_hi, inv_hi3, pri, bi, eps2, ci, thr; };
   struct FA { double a0, a1, udt, vsig, hdt; };
 
   // force_inv, kernels.cpp:155-172
   __device__ static FI for_i(double2 x, double2 vp, double h, double p, double rho,
-                             double rho_dh, double c, double div_v, double rot_v, double) {
+                             double rho_dh, double c, double div_v, double rot_v, double,
+                             FCold *) {
     FI I;
     I.x0 = x.x; I.x1 = x.y; I.v0 = vp.x; I.v1 = vp.y;
     I.hi = h;

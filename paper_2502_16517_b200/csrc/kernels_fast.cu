@@ -199,29 +199,42 @@ struct FastPolicy {
     o[5] = 4.0 * s.div * n3;
   }
 
+#if SPH_COLD
+  // per-i constants used only on the in-support path and at publish live in shared memory
+  // (one slot per lane), keeping the hot loop's register footprint small
+  struct FCold { double vx, vy, pri, mb3, K, ci, hi, pad; };
+  struct FI { double x, y, inv_hi, eps2; unsigned hiH2m1; FCold *cold; };
+#else
+  struct FCold { double pad; };
   struct FI { double x, y, vx, vy, inv_hi, eps2, pri, mb3, ci, hi, K; unsigned hiH2m1; };
+#endif
+
   struct FA { double ax, ay, udt, vsig, hdt, hdt0; };
 
   // force_inv (kernels.cpp:155-172); K = -4 N / h^3 multiplies every SPH pair term.
   __device__ static FI for_i(double2 x, double2 vp, double h, double p, double rho,
-                             double rho_dh, double c, double div_v, double rot_v, double) {
+                             double rho_dh, double c, double div_v, double rot_v, double,
+                             FCold *cold) {
     FI I;
-    I.x = x.x; I.y = x.y; I.vx = vp.x; I.vy = vp.y;
-    I.hi = h;
+    I.x = x.x; I.y = x.y;
     I.inv_hi = 1.0 / h;
     I.hiH2m1 = (unsigned)hi_word(6.25 * h * h) - 1u;
     I.eps2 = 0.01 * h * h;
     const double irho = 1.0 / rho;
-    I.pri = p * irho * irho * fma(0.5 * h * rho_dh, irho, 1.0);
+    const double pri = p * irho * irho * fma(0.5 * h * rho_dh, irho, 1.0);
     const double adiv = fabs(div_v);
-    I.ci = c;
     const double bi = adiv / (adiv + fabs(rot_v) + 0.0001 * c * I.inv_hi);
-    I.mb3 = -3.0 * bi;
-    I.K = -4.0 * kNorm2d * I.inv_hi * I.inv_hi * I.inv_hi;
+    const double K = -4.0 * kNorm2d * I.inv_hi * I.inv_hi * I.inv_hi;
+#if SPH_COLD
+    cold->vx = vp.x; cold->vy = vp.y; cold->pri = pri; cold->mb3 = -3.0 * bi; cold->K = K;
+    cold->ci = c; cold->hi = h;
+    I.cold = cold;
+#else
+    (void)cold;
+    I.vx = vp.x; I.vy = vp.y; I.pri = pri; I.mb3 = -3.0 * bi; I.K = K; I.ci = c; I.hi = h;
+#endif
     return I;
   }
-  // vsig accumulates max_j (c_j - 3 mu b_i) >= 0; -1 marks "no in-support pair" (the
-  // reference then keeps its initial +0.0, kernels.cpp:89)
   __device__ static FA for_zero(double h_dt) { return FA{0.0, 0.0, 0.0, -1.0, 0.0, h_dt}; }
 
   // tile terms: (m, grav*m, m*p/rho^2, m/rho)
@@ -236,12 +249,17 @@ struct FastPolicy {
   __device__ __forceinline__ static double for_in(const FI &I, double dx, double dy, double r2,
                                                   double2 vj, double2 mg, double2 pv, double cj,
                                                   FA &s) {
+#if SPH_COLD
+    const FCold &C = *I.cold;
+#else
+    const FI &C = I;
+#endif
     const double rinv = rsqrt_fast(r2);
     const double q = r2 * rinv * I.inv_hi;
     Spline sp;
     sp.template eval<false>(q);
     const double g = sp.E * rinv;
-    const double dvx = I.vx - vj.x, dvy = I.vy - vj.y;
+    const double dvx = C.vx - vj.x, dvy = C.vy - vj.y;
     const double dvdr = fma(dvx, dx, dvy * dy);
     const double gd = g * dvdr;
     s.udt = fma(mg.x, gd, s.udt);
@@ -250,9 +268,9 @@ struct FastPolicy {
     const double mu = (hi_word(dvdr) < 0 ? dvdr : 0.0) * rinv;
     // vsig = max_j (c_i + c_j - 3 mu b_i) = c_i + max_j (c_j - 3 mu b_i): fl(c_i + x) is
     // monotonic in x, so adding c_i once at the end gives the same value
-    const double vs = fma(mu, I.mb3, cj);
+    const double vs = fma(mu, C.mb3, cj);
     s.vsig = vs > s.vsig ? vs : s.vsig;
-    return fma(mg.x, I.pri, pv.x) * g * I.K;
+    return fma(mg.x, C.pri, pv.x) * g * C.K;
   }
 
   // Four pairs per step: distances and the softened gravity (every active pair,
@@ -299,11 +317,16 @@ struct FastPolicy {
   }
 
   __device__ static void for_publish(const FI &I, const FA &s, double o[5]) {
+#if SPH_COLD
+    const FCold &C = *I.cold;
+#else
+    const FI &C = I;
+#endif
     o[0] = s.ax;
     o[1] = s.ay;
-    o[2] = I.pri * I.K * s.udt;
-    o[3] = s.vsig < 0.0 ? 0.0 : I.ci + s.vsig;
-    o[4] = fma(-0.5 * I.hi * I.K, s.hdt, s.hdt0);
+    o[2] = C.pri * C.K * s.udt;
+    o[3] = s.vsig < 0.0 ? 0.0 : C.ci + s.vsig;
+    o[4] = fma(-0.5 * C.hi * C.K, s.hdt, s.hdt0);
   }
 };
 

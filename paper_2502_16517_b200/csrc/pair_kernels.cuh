@@ -35,6 +35,9 @@ constexpr double kDummyX = 1.0e30;
 #ifndef SPH_SPLINE3
 #define SPH_SPLINE3 0
 #endif
+#ifndef SPH_COLD
+#define SPH_COLD 0 // 1: FAST force keeps in-support-only per-i constants in shared memory (measured slower)
+#endif
 #ifndef SPH_FJ
 #define SPH_FJ 2 // force: pairs per interleaved gravity group
 #endif
@@ -341,6 +344,7 @@ template <class P, bool AOS, bool VIEW>
 __global__ void __launch_bounds__(kWarpsPerCta * 32, SPH_MINB_FOR) force_kernel(ForArgs A) {
   __shared__ ForTile tiles[kWarpsPerCta];
   __shared__ ActiveLayout lay[kWarpsPerCta];
+  __shared__ typename P::FCold cold[kWarpsPerCta * 32];
   const int w = warp_in_cta(), lane = lane_id();
   const int item_idx = blockIdx.x * kWarpsPerCta + w;
   if (item_idx >= A.n_items) return;
@@ -356,7 +360,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, SPH_MINB_FOR) force_kernel(
   const double hi = src.h(slot);
   typename P::FI I = P::for_i(xi, src.vp(slot), hi, src.pr(slot), src.rho(slot),
                               src.rho_dh(slot), src.c(slot), src.div_v(slot), src.rot_v(slot),
-                              A.grav);
+                              A.grav, &cold[threadIdx.x]);
   typename P::FA s = P::for_zero(src.h_dt(slot));
   const bool cull = A.boxes != nullptr;
   float ixlo = 0.f, ixhi = 0.f, iylo = 0.f, iyhi = 0.f, reach2 = 0.f;
