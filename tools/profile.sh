@@ -8,7 +8,7 @@ ncu --metrics gpu__time_duration.sum --clock-control none -c 600 --csv --log-fil
 ncu --set full --clock-control none --import-source on --kernel-name-base mangled \
     -k regex:force_kernelINS_10FastPolicy -c 1 -o gpurun_out/force_$TAG $B > /dev/null 2>&1
 ncu --set full --clock-control none --import-source on --kernel-name-base mangled \
-    -k regex:density_round_kernelINS_10FastPolicy -c 1 -o gpurun_out/density_$TAG $B > /dev/null 2>&1
+    -k regex:density_cull_kernelINS_10FastPolicy -c 1 -o gpurun_out/density_$TAG $B > /dev/null 2>&1
 ncu --set full --clock-control none --import-source on --kernel-name-base mangled \
     -k regex:"kick2_kernel|drift_kernel|kick1_kernel" -s 3 -c 3 -o gpurun_out/linear_$TAG $B > /dev/null 2>&1
 ls -la gpurun_out
