@@ -283,6 +283,7 @@ struct FastPolicy {
 #pragma unroll 1
     for (int j = 0; j < kTJ; j += G) {
       double dx[G], dy[G], r2[G], f[G];
+      bool in[G];
 #pragma unroll
       for (int k = 0; k < G; ++k) {
         const double2 xj = T.xy[j + k];
@@ -291,17 +292,60 @@ struct FastPolicy {
         if (MINIMG) { dx[k] -= round(dx[k]); dy[k] -= round(dy[k]); }
         r2[k] = fma(dx[k], dx[k], dy[k] * dy[k]);
         f[k] = T.mg[j + k].y * rsqrt3_fast(r2[k] + I.eps2);
+        in[k] = in_support(r2[k], I.hiH2m1);
       }
+#if SPH_MERGE
+      // one block for the whole group, chains interleaved; pairs outside the support are
+      // evaluated on a safe r2 and their contributions selected away
+      bool any = false;
+#pragma unroll
+      for (int k = 0; k < G; ++k) any |= in[k];
+      if (any) {
+#pragma unroll
+        for (int k = 0; k < G; ++k) {
+          const double add = for_in_masked(I, dx[k], dy[k], in[k] ? r2[k] : 1.0, in[k], T.vv[j + k],
+                                           T.mg[j + k], T.pv[j + k], T.c[j + k], s);
+          f[k] += add;
+        }
+      }
+#else
 #pragma unroll
       for (int k = 0; k < G; ++k)
-        if (in_support(r2[k], I.hiH2m1))
+        if (in[k])
           f[k] += for_in(I, dx[k], dy[k], r2[k], T.vv[j + k], T.mg[j + k], T.pv[j + k], T.c[j + k], s);
+#endif
 #pragma unroll
       for (int k = 0; k < G; ++k) {
         s.ax = fma(-f[k], dx[k], s.ax);
         s.ay = fma(-f[k], dy[k], s.ay);
       }
     }
+  }
+
+  // for_in with the contributions of a pair outside the support selected to zero
+  __device__ __forceinline__ static double for_in_masked(const FI &I, double dx, double dy,
+                                                         double r2, bool in, double2 vj,
+                                                         double2 mg, double2 pv, double cj,
+                                                         FA &s) {
+#if SPH_COLD
+    const FCold &C = *I.cold;
+#else
+    const FI &C = I;
+#endif
+    const double rinv = rsqrt_fast(r2);
+    const double q = r2 * rinv * I.inv_hi;
+    Spline sp;
+    sp.template eval<false>(q);
+    const double g = in ? sp.E * rinv : 0.0;
+    const double dvx = C.vx - vj.x, dvy = C.vy - vj.y;
+    const double dvdr = fma(dvx, dx, dvy * dy);
+    const double gd = g * dvdr;
+    s.udt = fma(mg.x, gd, s.udt);
+    s.hdt = fma(pv.y, gd, s.hdt);
+    const double mu = (hi_word(dvdr) < 0 ? dvdr : 0.0) * rinv;
+    const double vs = fma(mu, C.mb3, cj);
+    if (in && vs > s.vsig) s.vsig = vs;
+    return fma(mg.x, C.pri, pv.x) * g * C.K;
   }
 
   // Gravity only (chunk out of every lane's support): branch-free, shifted images.

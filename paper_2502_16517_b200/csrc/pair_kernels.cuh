@@ -38,6 +38,9 @@ constexpr double kDummyX = 1.0e30;
 #ifndef SPH_COLD
 #define SPH_COLD 0 // 1: FAST force keeps in-support-only per-i constants in shared memory (measured slower)
 #endif
+#ifndef SPH_MERGE
+#define SPH_MERGE 0 // 1: FAST force evaluates a pair group's SPH terms in one interleaved block
+#endif
 #ifndef SPH_FJ
 #define SPH_FJ 2 // force: pairs per interleaved gravity group
 #endif
