@@ -269,7 +269,9 @@ struct FastPolicy {
     // vsig = max_j (c_i + c_j - 3 mu b_i) = c_i + max_j (c_j - 3 mu b_i): fl(c_i + x) is
     // monotonic in x, so adding c_i once at the end gives the same value
     const double vs = fma(mu, C.mb3, cj);
-    s.vsig = vs > s.vsig ? vs : s.vsig;
+    // both >= 0 (or the -1 sentinel, whose bit pattern is negative): signed 64-bit integer
+    // order equals double order here, so the max runs on the ALU pipe
+    if (__double_as_longlong(vs) > __double_as_longlong(s.vsig)) s.vsig = vs;
     return fma(mg.x, C.pri, pv.x) * g * C.K;
   }
 
