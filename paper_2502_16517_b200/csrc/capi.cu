@@ -211,7 +211,9 @@ struct sph_ctx {
   DevBuf<unsigned char> rounds, again;
   DevBuf<float4> boxes;
   DevBuf<double2> jv_xy, jv_vv, jv_mg, jv_pv;
-  DevBuf<double> jv_m, jv_c;
+  DevBuf<double> jv_m, jv_c, jv2_x, jv2_y, jv2_gm;
+  DevBuf<double2> jv2_vv, jv2_pv, jv2_cm;
+  int force2 = 1; // FAST force on the resident SoA: issue-lean kernel (env SPH_B200_FORCE2=0: old)
   bool cull = true; // FAST density: spatial j order + chunk culling (env SPH_B200_CULL=0 disables)
   DevBuf<char> dense, cub_tmp;
   PinnedBuf h_stage, h_small;
@@ -250,6 +252,8 @@ struct sph_ctx {
     items_b.release(); hcur.release(); wc.release(); rounds.release(); dense.release();
     cub_tmp.release(); h_stage.release(); h_small.release(); owned.release();
     jv_xy.release(); jv_vv.release(); jv_mg.release(); jv_pv.release(); jv_m.release(); jv_c.release();
+    jv2_x.release(); jv2_y.release(); jv2_gm.release(); jv2_vv.release(); jv2_pv.release();
+    jv2_cm.release();
   }
 
   Geom geom() const {
@@ -453,6 +457,25 @@ struct sph_ctx {
     A.grav = par.grav;
     A.aos = aos.p;
     A.soa = soa;
+    if (!exact && cull && force2 && !use_aos && A.g.use_shift) {
+      // issue-lean kernel over the SoA mirror (spatial j order, far chunks gravity-only)
+      boxes.ensure((size_t)n / 32 + (size_t)ncells + 2);
+      launch_chunk_boxes(boxes.p, ilist.p, aos.p, soa, false, cell_begin.p, ncells, stream);
+      jv2_x.ensure(n); jv2_y.ensure(n); jv2_gm.ensure(n);
+      jv2_vv.ensure(n); jv2_pv.ensure(n); jv2_cm.ensure(n);
+      F2Args B{};
+      B.g = A.g;
+      B.items = items0.p;
+      B.list = ilist.p;
+      B.grav = par.grav;
+      B.soa = soa;
+      B.boxes = boxes.p;
+      B.jv = F2View{jv2_x.p, jv2_y.p, jv2_gm.p, jv2_vv.p, jv2_pv.p, jv2_cm.p};
+      launch_force2(B, n_items0, (int)n, stream);
+      launched(3);
+      stats.force_pairs = active_pairs;
+      return;
+    }
     if (!exact && cull) { // spatial j order + far-chunk gravity-only path
       boxes.ensure((size_t)n / 32 + (size_t)ncells + 2);
       launch_chunk_boxes(boxes.p, ilist.p, aos.p, soa, use_aos, cell_begin.p, ncells, stream);
@@ -800,6 +823,7 @@ int sph_create(int device, sph_ctx **out) {
   if (!ctx) return SPH_E_CUDA;
   ctx->device = device;
   if (const char *e = std::getenv("SPH_B200_CULL")) ctx->cull = std::atoi(e) != 0;
+  if (const char *e = std::getenv("SPH_B200_FORCE2")) ctx->force2 = std::atoi(e);
   int r = guarded(ctx, [&] {
     CK(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
     for (auto &e : ctx->ev) CK(cudaEventCreate(&e));

@@ -376,6 +376,281 @@ struct FastPolicy {
   }
 };
 
+// ---------------------------------------------------------------------------------------
+// Issue-lean FAST force sweep (force2). Same decomposition and numerics as force_kernel
+// with the FAST policy (one warp per item, lane = local i, chunks of the spatially ordered
+// active list, far chunks gravity-only), re-shaped so that the FP64 pipe, not instruction
+// issue, is the limit. ncu on force_kernel showed ~44 issued instructions per pair of
+// which only ~23 were FP64 (issue 63 %, FP64 pipe 65 %):
+//   * chunks are staged with cp.async straight into a double-buffered per-warp tile (no
+//     prefetch registers, no STS), the periodic image shift moves to the i side (xs, ys);
+//   * the tile keeps the gravity fields as separate x[], y[], gm[] arrays so one LDS.128
+//     serves two j's; the SPH fields are paired (vx,vy), (P,V), (c,m);
+//   * the spline piece is picked from a 3-row coefficient table in shared memory
+//     (s = c_off + sgn q, E = Horner(s)): 4 FP64 ops, no selects, no predicated
+//     correction for q < 0.5;
+//   * the series constants come from the kernel parameters (constant-bank operands), so
+//     they are not re-materialised with IMADs inside the loop.
+// ---------------------------------------------------------------------------------------
+struct __align__(16) F2Tile {
+  double x[kTJ], y[kTJ], gm[kTJ];
+  double2 vv[kTJ], pv[kTJ], cm[kTJ];
+  double2 spl[9]; // spline coefficient table (kSplE), one copy per tile so rows are
+                  // addressed relative to the tile pointer
+};
+
+// spline table rows (outer, mid, inner): {c_off, sgn}, {e3, e2}, {e1, e0};
+// s = c_off + sgn q, E(s) = ((e3 s + e2) s + e1) s + e0 (spline.hpp:12-41 as dW = -4 N E)
+__constant__ double2 kSplE[9] = {
+    {2.5, -1.0}, {1.0, 0.0}, {0.0, 0.0},   // q in [1.5, 2.5): E = (2.5 - q)^3
+    {1.5, -1.0}, {-4.0, 3.0}, {3.0, 1.0},  // q in [0.5, 1.5): s = 1.5 - q
+    {0.0, 1.0}, {-6.0, 0.0}, {7.5, 0.0},   // q in [0, 0.5):   E = -6 q^3 + 7.5 q
+};
+
+__device__ __forceinline__ void cp_async8(void *smem, const void *gmem) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async16(void *smem, const void *gmem) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N> __device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+
+// table row of q (q >= 0): 0 outer, 1 mid, 2 inner; interval tests on the high word
+// (exact: 0.5 and 1.5 have zero low words)
+__device__ __forceinline__ int spline_row(double q) {
+  const int hq = __double2hiint(q);
+  return (hq < 0x3FE00000 ? 1 : 0) + (hq < 0x3FF80000 ? 1 : 0);
+}
+
+#ifndef SPH_MINB_F2
+#define SPH_MINB_F2 5
+#endif
+
+// SPH part of force_pair (kernels.cpp:132-152) for one in-support pair: accumulates u_dt,
+// h_dt, v_sig and returns the SPH radial factor A*g (the caller applies K).
+struct F2I { double vx, vy, inv_hi, pri, mb3; };
+__device__ __forceinline__ double force2_sph(const F2I &I, const F2Tile &T, int j, double dx,
+                                             double dy, double r2, double k0375, double &udt,
+                                             double &hdt, double &vsig) {
+  const double y0 = rsqrt_seed(r2);
+  const double e = fma(-r2, y0 * y0, 1.0);
+  const double rinv = fma(y0, e * fma(e, k0375, 0.5), y0);
+  const double q = r2 * rinv * I.inv_hi;
+  const int hq = __double2hiint(q);
+  int row = hq < 0x3FF80000 ? 3 : 0; // q < 1.5
+  if (hq < 0x3FE00000) row = 6;      // q < 0.5
+  const double2 t0 = T.spl[row], t1 = T.spl[row + 1], t2 = T.spl[row + 2];
+  const double s = fma(t0.y, q, t0.x);
+  const double E = fma(fma(fma(t1.x, s, t1.y), s, t2.x), s, t2.y);
+  const double g = E * rinv;
+  const double2 vj = T.vv[j];
+  const double dvx = I.vx - vj.x, dvy = I.vy - vj.y;
+  const double dvdr = fma(dvx, dx, dvy * dy);
+  const double gd = g * dvdr;
+  const double2 cm = T.cm[j], pv = T.pv[j];
+  udt = fma(cm.y, gd, udt);
+  hdt = fma(pv.y, gd, hdt);
+  const double mu = (__double2hiint(dvdr) < 0 ? dvdr : 0.0) * rinv;
+  const double vs = fma(mu, I.mb3, cm.x);
+  if (__double_as_longlong(vs) > __double_as_longlong(vsig)) vsig = vs;
+  return fma(cm.y, I.pri, pv.x) * g;
+}
+
+__device__ __forceinline__ void force2_stage(F2Tile &T, const ActiveLayout &L, const F2View &jv,
+                                             int nb, int k, int lane) {
+  const int cnt = L.pre[nb + 1] - L.pre[nb];
+  const int q = k * kTJ + lane;
+  if (q < cnt) {
+    const int idx = L.base[nb] + q;
+    cp_async8(&T.x[lane], jv.x + idx);
+    cp_async8(&T.y[lane], jv.y + idx);
+    cp_async8(&T.gm[lane], jv.gm + idx);
+    cp_async16(&T.vv[lane], jv.vv + idx);
+    cp_async16(&T.pv[lane], jv.pv + idx);
+    cp_async16(&T.cm[lane], jv.cm + idx);
+  } else { // inert padding: gm = 0 and r2 beyond every support
+    T.x[lane] = kDummyX;
+    T.y[lane] = kDummyX;
+    T.gm[lane] = 0.0;
+    T.vv[lane] = make_double2(0.0, 0.0);
+    T.pv[lane] = make_double2(0.0, 0.0);
+    T.cm[lane] = make_double2(0.0, 0.0);
+  }
+  cp_async_commit();
+}
+
+template <int MINB>
+__global__ void __launch_bounds__(kWarpsPerCta * 32, MINB) force2_kernel(F2Args A) {
+  __shared__ F2Tile tiles[kWarpsPerCta][2];
+  __shared__ ActiveLayout lay[kWarpsPerCta];
+  const int w = warp_in_cta(), lane = lane_id();
+  const int item_idx = blockIdx.x * kWarpsPerCta + w;
+  if (item_idx >= A.n_items) return;
+  if (lane < 9) tiles[w][0].spl[lane] = tiles[w][1].spl[lane] = kSplE[lane];
+  ActiveLayout &L = lay[w];
+  const Item it = A.items[item_idx];
+  if (lane == 0) build_active(A.g, it.cell, L);
+  const bool live = lane < it.count;
+  const int slot = A.list[it.start + (live ? lane : 0)];
+  const double2 xi = A.soa.x[slot];
+  const double hi = A.soa.h[slot];
+  F2I I;
+  double eps2, K;
+  unsigned hiH2m1;
+  {
+    const FastPolicy::FI F =
+        FastPolicy::for_i(xi, A.soa.vp[slot], hi, A.soa.p[slot], A.soa.rho[slot],
+                          A.soa.rho_dh[slot], A.soa.c[slot], A.soa.div_v[slot],
+                          A.soa.rot_v[slot], A.grav, nullptr);
+    I = F2I{F.vx, F.vy, F.inv_hi, F.pri, F.mb3};
+    eps2 = F.eps2;
+    K = F.K;
+    hiH2m1 = F.hiH2m1;
+  }
+  double ax = 0.0, ay = 0.0, udt = 0.0, hdt = 0.0, vsig = -1.0;
+  const float ixlo = warp_min((float)xi.x), ixhi = warp_max((float)xi.x);
+  const float iylo = warp_min((float)xi.y), iyhi = warp_max((float)xi.y);
+  const float reach = warp_max((float)(2.5 * hi)) * (1.0f + 1e-5f) + 1e-6f;
+  const float reach2 = reach * reach;
+  const double k1875 = A.k1875, k0375 = A.k0375;
+  __syncwarp();
+
+  const int total = L.nch[L.n];
+  bool staged = false;
+  int buf = 0;
+  for (int g0 = 0; g0 < total; g0 += 32) {
+    // lane l classifies chunk g0 + l (stencil cell, chunk index, near/far), one ballot
+    const int g = g0 + lane;
+    int nb = 0, kk = 0;
+    const bool valid = g < total;
+    bool nr = false;
+    if (valid) {
+      chunk_locate(L, g, nb, kk);
+      nr = chunk_near(L, A.boxes, nb, kk, ixlo, ixhi, iylo, iyhi, reach2);
+    }
+    const unsigned nmask = __ballot_sync(0xffffffffu, nr);
+    unsigned todo = __ballot_sync(0xffffffffu, valid);
+    while (todo) {
+      const int b = __ffs(todo) - 1;
+      todo &= todo - 1;
+      const int cnb = __shfl_sync(0xffffffffu, nb, b), ck = __shfl_sync(0xffffffffu, kk, b);
+      const bool has_next = todo != 0u;
+      if (!staged) force2_stage(tiles[w][buf], L, A.jv, cnb, ck, lane);
+      if (has_next) {
+        const int bn = __ffs(todo) - 1;
+        const int nnb = __shfl_sync(0xffffffffu, nb, bn), nk = __shfl_sync(0xffffffffu, kk, bn);
+        force2_stage(tiles[w][buf ^ 1], L, A.jv, nnb, nk, lane);
+        cp_async_wait<1>();
+      } else {
+        cp_async_wait<0>();
+      }
+      staged = has_next;
+      __syncwarp();
+      const F2Tile &T = tiles[w][buf];
+      const double xs = xi.x - L.sx[cnb], ys = xi.y - L.sy[cnb]; // periodic image, i side
+      if ((nmask >> b) & 1u) {
+#pragma unroll 1
+        for (int j = 0; j < kTJ; j += 2) {
+          const double2 X = *reinterpret_cast<const double2 *>(&T.x[j]);
+          const double2 Y = *reinterpret_cast<const double2 *>(&T.y[j]);
+          const double2 G = *reinterpret_cast<const double2 *>(&T.gm[j]);
+          const double dx0 = xs - X.x, dy0 = ys - Y.x, dx1 = xs - X.y, dy1 = ys - Y.y;
+          const double r20 = fma(dx0, dx0, dy0 * dy0), r21 = fma(dx1, dx1, dy1 * dy1);
+          double f0, f1;
+          {
+            const double s0 = r20 + eps2, s1 = r21 + eps2;
+            const double y0 = rsqrt_seed(s0), y1 = rsqrt_seed(s1);
+            const double t0 = y0 * y0, t1 = y1 * y1;
+            const double e0 = fma(-s0, t0, 1.0), e1 = fma(-s1, t1, 1.0);
+            const double c0 = G.x * (t0 * y0), c1 = G.y * (t1 * y1);
+            f0 = fma(c0, e0 * fma(e0, k1875, 1.5), c0);
+            f1 = fma(c1, e1 * fma(e1, k1875, 1.5), c1);
+          }
+          if (in_support(r20, hiH2m1))
+            f0 = fma(K, force2_sph(I, T, j, dx0, dy0, r20, k0375, udt, hdt, vsig), f0);
+          if (in_support(r21, hiH2m1))
+            f1 = fma(K, force2_sph(I, T, j + 1, dx1, dy1, r21, k0375, udt, hdt, vsig), f1);
+          ax = fma(-f0, dx0, ax);
+          ay = fma(-f0, dy0, ay);
+          ax = fma(-f1, dx1, ax);
+          ay = fma(-f1, dy1, ay);
+        }
+      } else {
+#pragma unroll 1
+        for (int j = 0; j < kTJ; j += 4) {
+          double dx[4], dy[4], gm[4];
+          {
+            const double2 X0 = *reinterpret_cast<const double2 *>(&T.x[j]);
+            const double2 X1 = *reinterpret_cast<const double2 *>(&T.x[j + 2]);
+            const double2 Y0 = *reinterpret_cast<const double2 *>(&T.y[j]);
+            const double2 Y1 = *reinterpret_cast<const double2 *>(&T.y[j + 2]);
+            const double2 G0 = *reinterpret_cast<const double2 *>(&T.gm[j]);
+            const double2 G1 = *reinterpret_cast<const double2 *>(&T.gm[j + 2]);
+            dx[0] = xs - X0.x; dx[1] = xs - X0.y; dx[2] = xs - X1.x; dx[3] = xs - X1.y;
+            dy[0] = ys - Y0.x; dy[1] = ys - Y0.y; dy[2] = ys - Y1.x; dy[3] = ys - Y1.y;
+            gm[0] = G0.x; gm[1] = G0.y; gm[2] = G1.x; gm[3] = G1.y;
+          }
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const double s = fma(dx[u], dx[u], fma(dy[u], dy[u], eps2));
+            const double y0 = rsqrt_seed(s);
+            const double t = y0 * y0;
+            const double e = fma(-s, t, 1.0);
+            const double c = gm[u] * (t * y0);
+            const double f = fma(c, e * fma(e, k1875, 1.5), c);
+            ax = fma(-f, dx[u], ax);
+            ay = fma(-f, dy[u], ay);
+          }
+        }
+      }
+      __syncwarp();
+      buf ^= 1;
+    }
+  }
+  if (!live) return;
+  // publish (force_inv terms recomputed from memory: keeps c_i, h_i out of the loop)
+  const FastPolicy::FI F =
+      FastPolicy::for_i(xi, A.soa.vp[slot], hi, A.soa.p[slot], A.soa.rho[slot], A.soa.rho_dh[slot],
+                        A.soa.c[slot], A.soa.div_v[slot], A.soa.rot_v[slot], A.grav, nullptr);
+  FastPolicy::FA s{ax, ay, udt, vsig, hdt, A.soa.h_dt[slot]};
+  double o[5];
+  FastPolicy::for_publish(F, s, o);
+  A.soa.a[slot] = make_double2(o[0], o[1]);
+  A.soa.u_dt[slot] = o[2];
+  A.soa.v_sig[slot] = o[3];
+  A.soa.h_dt[slot] = o[4];
+}
+
+__global__ void jview_force2_kernel(F2View v, const int *ilist, SoaMirror f, int n, double grav) {
+  const int p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= n) return;
+  const int sj = ilist[p];
+  const double2 x = f.x[sj];
+  const double m = f.m[sj], rho = f.rho[sj];
+  const double4 d = FastPolicy::stage_force(m, rho, f.p[sj], grav); // (m, gm, P, V)
+  const_cast<double *>(v.x)[p] = x.x;
+  const_cast<double *>(v.y)[p] = x.y;
+  const_cast<double *>(v.gm)[p] = d.y;
+  const_cast<double2 *>(v.vv)[p] = f.vp[sj];
+  const_cast<double2 *>(v.pv)[p] = make_double2(d.z, d.w);
+  const_cast<double2 *>(v.cm)[p] = make_double2(f.c[sj], m);
+}
+
+void launch_force2(const F2Args &a, int n_items, int n, cudaStream_t s) {
+  if (n > 0) jview_force2_kernel<<<(n + 255) / 256, 256, 0, s>>>(a.jv, a.list, a.soa, n, a.grav);
+  if (n_items <= 0) return;
+  F2Args b = a;
+  b.n_items = n_items;
+  b.k1875 = 1.875;
+  b.k0375 = 0.375;
+  force2_kernel<SPH_MINB_F2><<<pair_grid(n_items), kWarpsPerCta * 32, 0, s>>>(b);
+}
+
 // j-view builders: gather the sweep's j fields into ilist order (+ hoisted invariants).
 template <bool AOS>
 __global__ void jview_density_kernel(double2 *xy, double2 *vv, double *m, const int *ilist,

@@ -95,6 +95,26 @@ struct ForArgs {
   JView jv;             // FAST: j-view in jlist order (null xy = gather from the mirror)
 };
 
+// Issue-lean FAST force (force2_kernel, kernels_fast.cu): j-view split for vector LDS.
+struct F2View {
+  const double *x, *y, *gm; // position, grav*m
+  const double2 *vv;        // v_pred
+  const double2 *pv;        // (P = m p / rho^2, V = m / rho)
+  const double2 *cm;        // (c, m)
+};
+
+struct F2Args {
+  Geom g;
+  const Item *items;
+  int n_items;
+  const int *list;
+  double grav;
+  SoaMirror soa;
+  const float4 *boxes;
+  F2View jv;
+  double k1875, k0375; // series constants (kernel parameters -> constant-bank operands)
+};
+
 // ---- j staging (gather one active record into the SoA tile) ----
 template <bool AOS> struct JSrc;
 template <> struct JSrc<true> {

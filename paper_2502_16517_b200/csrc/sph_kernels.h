@@ -6,12 +6,16 @@ namespace sphb {
 
 struct DenArgs;
 struct ForArgs;
+struct F2Args;
 
 // pair sweeps (pair_kernels.cuh instantiations)
 void launch_density_exact(const DenArgs &a, int n_items, bool aos, bool meanw, cudaStream_t s);
 void launch_force_exact(const ForArgs &a, int n_items, bool aos, cudaStream_t s);
 void launch_density_fast(const DenArgs &a, int n_items, bool aos, cudaStream_t s);
 void launch_force_fast(const ForArgs &a, int n_items, bool aos, cudaStream_t s);
+// issue-lean FAST force over the resident SoA mirror (builds its j-view first); needs the
+// per-stencil-cell periodic shift (nx, ny >= 5) and chunk boxes
+void launch_force2(const F2Args &a, int n_items, int n, cudaStream_t s);
 
 // FAST j-views (kernels_fast.cu): sweep j fields in ilist order with hoisted invariants
 void launch_jview_density(double2 *xy, double2 *vv, double *m, const int *ilist,
