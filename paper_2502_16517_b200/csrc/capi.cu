@@ -211,9 +211,10 @@ struct sph_ctx {
   DevBuf<unsigned char> rounds, again;
   DevBuf<float4> boxes;
   DevBuf<double2> jv_xy, jv_vv, jv_mg, jv_pv;
-  DevBuf<double> jv_m, jv_c, jv2_x, jv2_y, jv2_gm;
+  DevBuf<double> jv_m, jv_c, jv2_x, jv2_y, jv2_gm, jv2_m;
   DevBuf<double2> jv2_vv, jv2_pv, jv2_cm;
   int force2 = 1; // FAST force on the resident SoA: issue-lean kernel (env SPH_B200_FORCE2=0: old)
+  int den_js0 = 1, den_js1 = 2; // lean density: lanes per particle in round 0 / rounds >= 1
   bool cull = true; // FAST density: spatial j order + chunk culling (env SPH_B200_CULL=0 disables)
   DevBuf<char> dense, cub_tmp;
   PinnedBuf h_stage, h_small;
@@ -253,7 +254,7 @@ struct sph_ctx {
     cub_tmp.release(); h_stage.release(); h_small.release(); owned.release();
     jv_xy.release(); jv_vv.release(); jv_mg.release(); jv_pv.release(); jv_m.release(); jv_c.release();
     jv2_x.release(); jv2_y.release(); jv2_gm.release(); jv2_vv.release(); jv2_pv.release();
-    jv2_cm.release();
+    jv2_cm.release(); jv2_m.release();
   }
 
   Geom geom() const {
@@ -384,19 +385,40 @@ struct sph_ctx {
     if (!exact && !meanw && cull) {
       boxes.ensure((size_t)n / 32 + (size_t)ncells + 2);
       launch_chunk_boxes(boxes.p, ilist.p, aos.p, soa, use_aos, cell_begin.p, ncells, stream);
-      jv_xy.ensure(n); jv_vv.ensure(n); jv_m.ensure(n);
-      launch_jview_density(jv_xy.p, jv_vv.p, jv_m.p, ilist.p, aos.p, soa, use_aos, (int)n, stream);
-      launched(2);
+      launched();
       A.boxes = boxes.p;
       A.jlist = ilist.p;
-      A.jv.xy = jv_xy.p;
-      A.jv.vv = jv_vv.p;
-      A.jv.m = jv_m.p;
+      if (force2 && !use_aos && A.g.use_shift) { // issue-lean density over the SoA mirror
+        jv2_x.ensure(n); jv2_y.ensure(n); jv2_m.ensure(n); jv2_vv.ensure(n);
+        A.jv2 = D2View{jv2_x.p, jv2_y.p, jv2_m.p, jv2_vv.p};
+        launch_jview_density2(A.jv2, ilist.p, soa, (int)n, stream);
+      } else {
+        jv_xy.ensure(n); jv_vv.ensure(n); jv_m.ensure(n);
+        launch_jview_density(jv_xy.p, jv_vv.p, jv_m.p, ilist.p, aos.p, soa, use_aos, (int)n, stream);
+        A.jv.xy = jv_xy.p;
+        A.jv.vv = jv_vv.p;
+        A.jv.m = jv_m.p;
+      }
+      launched();
     }
+    const bool lean = A.jv2.x != nullptr;
+    const int js0 = lean ? std::max(1, std::min(4, den_js0)) : 1;
+    const int js1 = lean ? std::max(1, std::min(4, den_js1)) : 1;
     const Item *items = items0.p;
     const int *list = ilist.p;
     const int *cnt_cur = cnt.p; // entries of `list` per cell (round 0: every local)
     int nitems = n_items0;
+    items_a.ensure((size_t)ncells + (size_t)n / (kTI / js1) + 1);
+    items_b.ensure((size_t)ncells + (size_t)n / (kTI / std::max(js0, js1)) + 1);
+    if (js0 > 1) { // round-0 items of 32/js0 particles
+      launch_make_items(items_b.p, scalars.p, pairs_dev.p, cnt.p, cell_begin.p, na_cell.p,
+                        cell_order.p, ncells, stream, kTI / js0);
+      launched();
+      CK(cudaMemcpyAsync(h_small.p, scalars.p, sizeof(int), cudaMemcpyDeviceToHost, stream));
+      CK(cudaStreamSynchronize(stream));
+      nitems = *(int *)h_small.p;
+      items = items_b.p;
+    }
     int64_t pairs = active_pairs, pairs_total = 0;
     int max_round = 0;
     for (double &v : round_ms) v = 0.0;
@@ -407,6 +429,7 @@ struct sph_ctx {
       A.items = items;
       A.list = list;
       A.round = r;
+      A.jslices = r == 0 ? js0 : js1;
       if (meanw) {
         launch_density_exact(A, nitems, use_aos, true, stream);
         launched();
@@ -419,7 +442,7 @@ struct sph_ctx {
       launch_compact_pending(pend_out, cnt_out, list, cnt_cur, again.p, cell_begin.p, ncells,
                              stream);
       launch_make_items(items_next, scalars.p, pairs_dev.p, cnt_out, cell_begin.p, na_cell.p,
-                        cell_order.p, ncells, stream);
+                        cell_order.p, ncells, stream, kTI / js1);
       launched(3);
       pairs_total += pairs;
       max_round = r + 1;
@@ -824,6 +847,8 @@ int sph_create(int device, sph_ctx **out) {
   ctx->device = device;
   if (const char *e = std::getenv("SPH_B200_CULL")) ctx->cull = std::atoi(e) != 0;
   if (const char *e = std::getenv("SPH_B200_FORCE2")) ctx->force2 = std::atoi(e);
+  if (const char *e = std::getenv("SPH_B200_DEN_JS0")) ctx->den_js0 = std::atoi(e);
+  if (const char *e = std::getenv("SPH_B200_DEN_JS1")) ctx->den_js1 = std::atoi(e);
   int r = guarded(ctx, [&] {
     CK(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
     for (auto &e : ctx->ev) CK(cudaEventCreate(&e));

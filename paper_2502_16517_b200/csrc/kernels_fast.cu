@@ -626,6 +626,217 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, MINB) force2_kernel(F2Args 
   A.soa.h_dt[slot] = o[4];
 }
 
+// ---------------------------------------------------------------------------------------
+// Issue-lean culled FAST density round (density2): density_cull_kernel's decomposition
+// (far chunks skipped, spatial j order, h-iteration rounds) with force2's staging (cp.async
+// double buffer, split x[]/y[] tile) and a 3-piece coefficient table for W and dW.
+// ---------------------------------------------------------------------------------------
+struct __align__(16) D2Tile {
+  double x[kTJ], y[kTJ], m[kTJ];
+  double2 vv[kTJ];
+  double2 spl[18]; // rows (outer, mid, inner) x {c_off, sgn}, {e3, e2}, {e1, e0}, {c4, c3}, {c2, c1}, {c0, 0}
+};
+
+// W(q) = N P(s), dW/dq = -4 N E(s) with s = c_off + sgn q (spline.hpp:12-41)
+__constant__ double2 kSplPE[18] = {
+    {2.5, -1.0}, {1.0, 0.0}, {0.0, 0.0}, {1.0, 0.0}, {0.0, 0.0}, {0.0, 0.0},         // s^4
+    {1.5, -1.0}, {-4.0, 3.0}, {3.0, 1.0}, {-4.0, 4.0}, {6.0, 4.0}, {1.0, 0.0},       // mid
+    {0.0, 1.0}, {-6.0, 0.0}, {7.5, 0.0}, {6.0, 0.0}, {-15.0, 0.0}, {14.375, 0.0},    // inner
+};
+
+__device__ __forceinline__ void density2_stage(D2Tile &T, const ActiveLayout &L, const D2View &jv,
+                                               int nb, int k, int lane) {
+  const int cnt = L.pre[nb + 1] - L.pre[nb];
+  const int q = k * kTJ + lane;
+  if (q < cnt) {
+    const int idx = L.base[nb] + q;
+    cp_async8(&T.x[lane], jv.x + idx);
+    cp_async8(&T.y[lane], jv.y + idx);
+    cp_async8(&T.m[lane], jv.m + idx);
+    cp_async16(&T.vv[lane], jv.vv + idx);
+  } else { // inert padding: beyond every support
+    T.x[lane] = kDummyX;
+    T.y[lane] = kDummyX;
+    T.m[lane] = 0.0;
+    T.vv[lane] = make_double2(0.0, 0.0);
+  }
+  cp_async_commit();
+}
+
+// density_pair (kernels.cpp:97-119) for one in-support pair, on FastPolicy's scaled sums
+__device__ __forceinline__ void density2_pair(const FastPolicy::DI &I, const D2Tile &T, int j,
+                                              double dx, double dy, double r2, double k0375,
+                                              FastPolicy::DA &s) {
+  const double y0 = rsqrt_seed(r2);
+  const double e = fma(-r2, y0 * y0, 1.0);
+  const double rinv = fma(y0, e * fma(e, k0375, 0.5), y0);
+  const double q = r2 * rinv * I.inv_h;
+  const int hq = __double2hiint(q);
+  int row = hq < 0x3FF80000 ? 6 : 0; // q < 1.5
+  if (hq < 0x3FE00000) row = 12;     // q < 0.5
+  const double2 t0 = T.spl[row], t1 = T.spl[row + 1], t2 = T.spl[row + 2];
+  const double2 t3 = T.spl[row + 3], t4 = T.spl[row + 4], t5 = T.spl[row + 5];
+  const double sv = fma(t0.y, q, t0.x);
+  const double E = fma(fma(fma(t1.x, sv, t1.y), sv, t2.x), sv, t2.y);
+  const double P = fma(fma(fma(fma(t3.x, sv, t3.y), sv, t4.x), sv, t4.y), sv, t5.x);
+  const double mj = T.m[j];
+  s.rho = fma(mj, P, s.rho);
+  s.w += P;
+  const double mE = mj * E;
+  s.qe = fma(q, mE, s.qe);
+  const double fac = mE * rinv;
+  const double2 vj = T.vv[j];
+  const double dvx = I.vx - vj.x, dvy = I.vy - vj.y;
+  s.div = fma(fac, fma(dvx, dx, dvy * dy), s.div);
+  s.rot = fma(fac, fma(dvx, dy, -dvy * dx), s.rot);
+}
+
+#ifndef SPH_MINB_D2
+#define SPH_MINB_D2 5
+#endif
+
+// JS lanes share one local particle i (j-slices): the warp holds 32/JS particles, which
+// keeps its bounding box small when the locals are sparse (pending particles of the
+// h-iteration rounds >= 1, ~12 % of a cell), so culling and the in-support union stay as
+// tight as in round 0. Lane slice q takes j = q, q + JS, ... of each tile; the JS partial
+// sums are combined with shuffles at the end.
+template <int MINB, int JS>
+__global__ void __launch_bounds__(kWarpsPerCta * 32, MINB) density2_kernel(DenArgs A) {
+  __shared__ D2Tile tiles[kWarpsPerCta][2];
+  __shared__ ActiveLayout lay[kWarpsPerCta];
+  const int w = warp_in_cta(), lane = lane_id();
+  const int item_idx = blockIdx.x * kWarpsPerCta + w;
+  if (item_idx >= A.n_items) return;
+  if (lane < 18) tiles[w][0].spl[lane] = tiles[w][1].spl[lane] = kSplPE[lane];
+  ActiveLayout &L = lay[w];
+  const Item it = A.items[item_idx];
+  if (lane == 0) build_active(A.g, it.cell, L);
+  const int iw = lane / JS, qs = lane % JS;
+  const bool live = iw < it.count;
+  const int slot = A.list[it.start + (live ? iw : 0)];
+  const double2 xi = A.soa.x[slot], vi = A.soa.vp[slot];
+  const double h = (A.round == 0) ? A.soa.h[slot] : A.hcur[slot];
+  const FastPolicy::DI I = FastPolicy::den_i(xi.x, xi.y, vi.x, vi.y, h);
+  FastPolicy::DA s = FastPolicy::den_zero();
+  const float ixlo = warp_min((float)xi.x), ixhi = warp_max((float)xi.x);
+  const float iylo = warp_min((float)xi.y), iyhi = warp_max((float)xi.y);
+  const float reach = warp_max((float)(2.5 * h)) * (1.0f + 1e-5f) + 1e-6f;
+  const float reach2 = reach * reach;
+  const double k0375 = A.k0375;
+  __syncwarp();
+
+  const int total = L.nch[L.n];
+  bool staged = false;
+  int buf = 0;
+  for (int g0 = 0; g0 < total; g0 += 32) {
+    const int g = g0 + lane;
+    int nb = 0, kk = 0;
+    bool nr = false;
+    if (g < total) {
+      chunk_locate(L, g, nb, kk);
+      nr = chunk_near(L, A.boxes, nb, kk, ixlo, ixhi, iylo, iyhi, reach2);
+    }
+    unsigned todo = __ballot_sync(0xffffffffu, nr); // far chunks hold no in-support pair
+    while (todo) {
+      const int b = __ffs(todo) - 1;
+      todo &= todo - 1;
+      const int cnb = __shfl_sync(0xffffffffu, nb, b), ck = __shfl_sync(0xffffffffu, kk, b);
+      const bool has_next = todo != 0u;
+      if (!staged) density2_stage(tiles[w][buf], L, A.jv2, cnb, ck, lane);
+      if (has_next) {
+        const int bn = __ffs(todo) - 1;
+        const int nnb = __shfl_sync(0xffffffffu, nb, bn), nk = __shfl_sync(0xffffffffu, kk, bn);
+        density2_stage(tiles[w][buf ^ 1], L, A.jv2, nnb, nk, lane);
+        cp_async_wait<1>();
+      } else {
+        cp_async_wait<0>();
+      }
+      staged = has_next;
+      __syncwarp();
+      const D2Tile &T = tiles[w][buf];
+      const double xs = xi.x - L.sx[cnb], ys = xi.y - L.sy[cnb]; // periodic image, i side
+      if constexpr (JS == 1) {
+#pragma unroll 1
+        for (int j = 0; j < kTJ; j += 4) {
+          double dx[4], dy[4], r2[4];
+          {
+            const double2 X0 = *reinterpret_cast<const double2 *>(&T.x[j]);
+            const double2 X1 = *reinterpret_cast<const double2 *>(&T.x[j + 2]);
+            const double2 Y0 = *reinterpret_cast<const double2 *>(&T.y[j]);
+            const double2 Y1 = *reinterpret_cast<const double2 *>(&T.y[j + 2]);
+            dx[0] = xs - X0.x; dx[1] = xs - X0.y; dx[2] = xs - X1.x; dx[3] = xs - X1.y;
+            dy[0] = ys - Y0.x; dy[1] = ys - Y0.y; dy[2] = ys - Y1.x; dy[3] = ys - Y1.y;
+          }
+#pragma unroll
+          for (int u = 0; u < 4; ++u) r2[u] = fma(dx[u], dx[u], dy[u] * dy[u]);
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+            if (in_support(r2[u], I.hiH2m1)) density2_pair(I, T, j + u, dx[u], dy[u], r2[u], k0375, s);
+        }
+      } else {
+        constexpr int U = (kTJ / JS) < 4 ? (kTJ / JS) : 4;
+#pragma unroll 1
+        for (int t = 0; t < kTJ / JS; t += U) {
+          double dx[U], dy[U], r2[U];
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            const int j = qs + JS * (t + u);
+            dx[u] = xs - T.x[j];
+            dy[u] = ys - T.y[j];
+            r2[u] = fma(dx[u], dx[u], dy[u] * dy[u]);
+          }
+#pragma unroll
+          for (int u = 0; u < U; ++u)
+            if (in_support(r2[u], I.hiH2m1))
+              density2_pair(I, T, qs + JS * (t + u), dx[u], dy[u], r2[u], k0375, s);
+        }
+      }
+      __syncwarp();
+      buf ^= 1;
+    }
+  }
+  if constexpr (JS > 1) { // combine the j-slices of each particle
+#pragma unroll
+    for (int o = 1; o < JS; o <<= 1) {
+      s.rho += __shfl_xor_sync(0xffffffffu, s.rho, o);
+      s.w += __shfl_xor_sync(0xffffffffu, s.w, o);
+      s.qe += __shfl_xor_sync(0xffffffffu, s.qe, o);
+      s.rot += __shfl_xor_sync(0xffffffffu, s.rot, o);
+      s.div += __shfl_xor_sync(0xffffffffu, s.div, o);
+    }
+  }
+  if (!live || qs != 0) return;
+  double hn = h;
+  const int st = FastPolicy::den_step(s, hn, A.target, A.h_max, A.round);
+  A.again[it.start + iw] = (unsigned char)(st == 0);
+  if (st == 0) {
+    A.hcur[slot] = hn;
+    return;
+  }
+  double o[6];
+  FastPolicy::den_publish(s, h, A.soa.m[slot], o);
+  if (A.rounds_out) A.rounds_out[slot] = (unsigned char)(A.round + 1);
+  A.soa.h[slot] = o[0]; A.soa.rho[slot] = o[1]; A.soa.wcount[slot] = o[2];
+  A.soa.rho_dh[slot] = o[3]; A.soa.rot_v[slot] = o[4]; A.soa.div_v[slot] = o[5];
+  if (st == 2) A.soa.flags[slot] += 1;
+}
+
+__global__ void jview_density2_kernel(D2View v, const int *ilist, SoaMirror f, int n) {
+  const int p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= n) return;
+  const int sj = ilist[p];
+  const double2 x = f.x[sj];
+  const_cast<double *>(v.x)[p] = x.x;
+  const_cast<double *>(v.y)[p] = x.y;
+  const_cast<double *>(v.m)[p] = f.m[sj];
+  const_cast<double2 *>(v.vv)[p] = f.vp[sj];
+}
+
+void launch_jview_density2(const D2View &v, const int *ilist, const SoaMirror &f, int n,
+                           cudaStream_t s) {
+  if (n > 0) jview_density2_kernel<<<(n + 255) / 256, 256, 0, s>>>(v, ilist, f, n);
+}
+
 __global__ void jview_force2_kernel(F2View v, const int *ilist, SoaMirror f, int n, double grav) {
   const int p = blockIdx.x * blockDim.x + threadIdx.x;
   if (p >= n) return;
@@ -705,7 +916,14 @@ void launch_density_fast(const DenArgs &a, int n_items, bool aos, cudaStream_t s
   DenArgs b = a;
   b.n_items = n_items;
   const int G = pair_grid(n_items), B = kWarpsPerCta * 32;
-  if (b.boxes && b.jlist) {
+  if (b.boxes && b.jlist && b.jv2.x && !aos) {
+    b.k0375 = 0.375;
+    switch (b.jslices) {
+    case 2: density2_kernel<SPH_MINB_D2, 2><<<G, B, 0, s>>>(b); break;
+    case 4: density2_kernel<SPH_MINB_D2, 4><<<G, B, 0, s>>>(b); break;
+    default: density2_kernel<SPH_MINB_D2, 1><<<G, B, 0, s>>>(b); break;
+    }
+  } else if (b.boxes && b.jlist) {
     if (aos) density_cull_kernel<FastPolicy, true><<<G, B, 0, s>>>(b);
     else density_cull_kernel<FastPolicy, false><<<G, B, 0, s>>>(b);
   } else {

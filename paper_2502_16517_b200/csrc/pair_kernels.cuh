@@ -64,6 +64,12 @@ struct JView {
   const double *c;        // force: sound speed
 };
 
+// Issue-lean FAST density (density2_kernel, kernels_fast.cu): j-view split for vector LDS.
+struct D2View {
+  const double *x, *y, *m; // position, mass
+  const double2 *vv;       // v_pred
+};
+
 struct DenArgs {
   Geom g;
   const Item *items;
@@ -80,6 +86,9 @@ struct DenArgs {
   const int *jlist;     // culled FAST sweep: cell-major slots in spatial order (ilist)
   const float4 *boxes;  // culled FAST sweep: bounding box of each 32-chunk of jlist
   JView jv;             // culled FAST sweep: j-view in jlist order
+  D2View jv2;           // issue-lean FAST sweep (resident SoA): split j-view (x null = off)
+  double k0375;         // series constant (kernel parameter -> constant-bank operand)
+  int jslices;          // density2: lanes per local particle (1, 2, 4); items hold 32/jslices
 };
 
 struct ForArgs {
