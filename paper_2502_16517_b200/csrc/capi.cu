@@ -177,6 +177,11 @@ struct Mt64 {
 struct sph_ctx {
   int device = 0;
   cudaStream_t stream = nullptr;
+  // pipelined end-to-end step (sph_step_host): force chunks on two streams, per-chunk
+  // kick2 + host-order compaction on `post`, device->host copies on `copy`
+  cudaStream_t fs[2]{}, post = nullptr, copy = nullptr;
+  cudaEvent_t pev[40]{};
+  int pipeline = 1; // env SPH_B200_PIPELINE=0: serial force -> kick2 -> download
   std::string err;
   int numerics = SPH_NUMERICS_FAST;
   int layout = SPH_LAYOUT_FROM_PATH;
@@ -206,7 +211,8 @@ struct sph_ctx {
   DevBuf<unsigned char> owned;
   bool has_owned = false;
   DevBuf<int> cell_order, cell_order_in;
-  DevBuf<Item> items0, items_a, items_b;
+  DevBuf<Item> items0, items_a, items_b, items_g;
+  DevBuf<int> hdep;
   DevBuf<double> hcur, wc;
   DevBuf<unsigned char> rounds, again;
   DevBuf<float4> boxes;
@@ -233,6 +239,12 @@ struct sph_ctx {
   double round_ms[4]{};
 
   ~sph_ctx() {
+    for (auto &e : pev)
+      if (e) cudaEventDestroy(e);
+    for (auto &q : fs)
+      if (q) cudaStreamDestroy(q);
+    if (post) cudaStreamDestroy(post);
+    if (copy) cudaStreamDestroy(copy);
     for (auto &e : ev)
       if (e) cudaEventDestroy(e);
     for (auto &e : rev)
@@ -252,6 +264,7 @@ struct sph_ctx {
     cell_order.release(); cell_order_in.release(); items0.release(); items_a.release();
     items_b.release(); hcur.release(); wc.release(); rounds.release(); dense.release();
     cub_tmp.release(); h_stage.release(); h_small.release(); owned.release();
+    items_g.release(); hdep.release();
     jv_xy.release(); jv_vv.release(); jv_mg.release(); jv_pv.release(); jv_m.release(); jv_c.release();
     jv2_x.release(); jv2_y.release(); jv2_gm.release(); jv2_vv.release(); jv2_pv.release();
     jv2_cm.release(); jv2_m.release();
@@ -518,6 +531,148 @@ struct sph_ctx {
     else launch_force_fast(A, n_items0, use_aos, stream);
     launched();
     stats.force_pairs = active_pairs;
+  }
+
+  bool can_pipeline(void *const *recs) const {
+    return pipeline && numerics == SPH_NUMERICS_FAST && cull && force2 && !has_owned &&
+           mode_for(SPH_PATH_AOS_BASELINE) == SPH_LAYOUT_RESIDENT && nx >= 5 && ny >= 5 &&
+           n >= 4096 && contiguous(recs);
+  }
+
+  // force -> kick2 -> download for host records at `host` (contiguous, bound order), with
+  // the device->host copy of finished particles overlapping the rest of the force sweep.
+  // The force sweep runs as K chunks of whole cells in grid (slot) order; chunk f finishes
+  // slots [sb[f], sb[f+1]). After each chunk, kick2 and the host-order compaction of its
+  // slots run on `post`; host chunk g (a contiguous range of records) is copied as soon as
+  // the last force chunk holding one of its particles is through `post`. Times (ms):
+  // out[0] force (first chunk start -> last chunk end), out[1] the exposed tail.
+  void force_kick2_download_pipelined(void *host, const Params &par, float out[2]) {
+    constexpr int K = 8, G = 64;
+    if (!fs[0]) {
+      for (auto &q : fs) CK(cudaStreamCreateWithFlags(&q, cudaStreamNonBlocking));
+      // kick2/compaction CTAs must not queue behind the force chunks' CTAs
+      int lo = 0, hi = 0;
+      CK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+      CK(cudaStreamCreateWithPriority(&post, cudaStreamNonBlocking, hi));
+      CK(cudaStreamCreateWithPriority(&copy, cudaStreamNonBlocking, hi));
+      for (auto &e : pev) CK(cudaEventCreate(&e));
+    }
+    make_soa_current();
+    // grid-order items and the per-cell item prefix (host)
+    items_g.ensure((size_t)ncells + (size_t)n / kTI + 1);
+    launch_make_items(items_g.p, scalars.p, pairs_dev.p, cnt.p, cell_begin.p, na_cell.p, nullptr,
+                      ncells, stream);
+    launched();
+    std::vector<int> cb(ncells + 1);
+    CK(cudaMemcpyAsync(cb.data(), cell_begin.p, sizeof(int) * (ncells + 1), cudaMemcpyDeviceToHost,
+                       stream));
+    CK(cudaStreamSynchronize(stream));
+    std::vector<int> kpre(ncells + 1, 0); // items in cells < c
+    for (int c = 0; c < ncells; ++c) kpre[c + 1] = kpre[c] + (cb[c + 1] - cb[c] + kTI - 1) / kTI;
+    // K chunks of whole cells with ~equal particle counts
+    ChunkBounds B{};
+    B.k = K;
+    int kb[K + 1];
+    {
+      int c = 0;
+      for (int f = 0; f <= K; ++f) {
+        const long long target = (long long)n * f / K;
+        while (c < ncells && cb[c] < target) ++c;
+        if (f == K) c = ncells;
+        B.s[f] = cb[c];
+        kb[f] = kpre[c];
+      }
+    }
+    // host chunk -> last force chunk
+    const int hsz = (int)((n + G - 1) / G);
+    hdep.ensure(G);
+    CK(cudaMemsetAsync(hdep.p, 0, sizeof(int) * G, stream));
+    launch_host_chunk_dep(hdep.p, host_idx.p, (int)n, hsz, B, stream);
+    launched();
+    int dep[G];
+    CK(cudaMemcpyAsync(dep, hdep.p, sizeof dep, cudaMemcpyDeviceToHost, stream));
+    // force prologue: chunk boxes + j-view (main stream)
+    boxes.ensure((size_t)n / 32 + (size_t)ncells + 2);
+    launch_chunk_boxes(boxes.p, ilist.p, aos.p, soa, false, cell_begin.p, ncells, stream);
+    jv2_x.ensure(n); jv2_y.ensure(n); jv2_gm.ensure(n);
+    jv2_vv.ensure(n); jv2_pv.ensure(n); jv2_cm.ensure(n);
+    F2Args A{};
+    A.g = geom();
+    A.list = ilist.p;
+    A.grav = par.grav;
+    A.soa = soa;
+    A.boxes = boxes.p;
+    A.jv = F2View{jv2_x.p, jv2_y.p, jv2_gm.p, jv2_vv.p, jv2_pv.p, jv2_cm.p};
+    A.items = items_g.p;
+    launch_force2(A, 0, (int)n, stream); // j-view only
+    launched(2);
+    CK(cudaStreamSynchronize(stream)); // dep[] on the host
+    cudaEvent_t e_pre = pev[0];
+    CK(cudaEventRecord(e_pre, stream));
+    dense.ensure((size_t)n * SPH_RECORD_SIZE);
+    Particle *dn = reinterpret_cast<Particle *>(dense.p);
+    for (int f = 0; f < K; ++f) {
+      cudaStream_t q = fs[f & 1];
+      if (f < 2) CK(cudaStreamWaitEvent(q, e_pre, 0));
+      A.items = items_g.p + kb[f];
+      launch_force2(A, kb[f + 1] - kb[f], 0, q);
+      launched();
+      CK(cudaEventRecord(pev[1 + f], q)); // force chunk f done
+      CK(cudaStreamWaitEvent(post, pev[1 + f], 0));
+      const int s0 = B.s[f], s1 = B.s[f + 1];
+      if (s1 > s0) {
+        SoaMirror o = soa_at(s0);
+        launch_linear(SPH_KICK2, false, aos.p + s0, o, s1 - s0, par, post);
+        launch_compact_soa(dn, aos.p, soa, host_idx.p, s0, s1, post);
+        launched(2);
+      }
+      CK(cudaEventRecord(pev[1 + K + f], post)); // slots of chunk f final in `dense`
+    }
+    // copies in order of readiness
+    int order[G];
+    for (int g = 0; g < G; ++g) order[g] = g;
+    std::stable_sort(order, order + G, [&](int a, int b) { return dep[a] < dep[b]; });
+    int waited = -1;
+    for (int t = 0; t < G; ++t) {
+      const int g = order[t];
+      const int64_t h0 = (int64_t)g * hsz, h1 = std::min<int64_t>(n, h0 + hsz);
+      if (h1 <= h0) continue;
+      if (dep[g] > waited) {
+        CK(cudaStreamWaitEvent(copy, pev[1 + K + dep[g]], 0));
+        waited = dep[g];
+      }
+      CK(cudaMemcpyAsync(static_cast<char *>(host) + h0 * SPH_RECORD_SIZE,
+                         reinterpret_cast<char *>(dn + h0), (size_t)(h1 - h0) * SPH_RECORD_SIZE,
+                         cudaMemcpyDeviceToHost, copy));
+    }
+    // join: the main stream waits for the last force chunks, post and copy
+    CK(cudaEventRecord(pev[2 * K + 1], copy));
+    CK(cudaEventRecord(pev[2 * K + 2], post));
+    CK(cudaStreamWaitEvent(stream, pev[K - 1], 0));
+    CK(cudaStreamWaitEvent(stream, pev[K], 0));
+    CK(cudaStreamWaitEvent(stream, pev[2 * K + 1], 0));
+    CK(cudaStreamWaitEvent(stream, pev[2 * K + 2], 0));
+    CK(cudaEventRecord(pev[2 * K + 3], stream));
+    CK(cudaEventSynchronize(pev[2 * K + 3]));
+    float a0 = 0, a1 = 0, t = 0;
+    CK(cudaEventElapsedTime(&a0, e_pre, pev[K - 1])); // the last chunk of each force stream
+    CK(cudaEventElapsedTime(&a1, e_pre, pev[K]));
+    CK(cudaEventElapsedTime(&t, e_pre, pev[2 * K + 3]));
+    out[0] = std::max(a0, a1);
+    out[1] = t - out[0]; // exposed kick2 / copy tail
+    stats.force_pairs = active_pairs;
+    soa_ahead = true;
+    soa_valid = true;
+    dirty = 0;
+  }
+
+  SoaMirror soa_at(int s0) const {
+    SoaMirror o = soa;
+    o.x += s0; o.v += s0; o.vp += s0; o.a += s0; o.m += s0; o.rho += s0; o.p += s0; o.u += s0;
+    o.u_pred += s0; o.u_dt += s0; o.c += s0; o.h += s0; o.wcount += s0; o.rho_dh += s0;
+    o.rot_v += s0; o.div_v += s0; o.v_sig += s0; o.h_dt += s0; o.dt_next += s0; o.dbg0 += s0;
+    o.frozen += s0; o.moved += s0; o.flags += s0;
+    return o;
   }
 
   // One sweep on the device. Events: ev[0..3] bracket prologue / compute / epilogue.
@@ -847,6 +1002,7 @@ int sph_create(int device, sph_ctx **out) {
   ctx->device = device;
   if (const char *e = std::getenv("SPH_B200_CULL")) ctx->cull = std::atoi(e) != 0;
   if (const char *e = std::getenv("SPH_B200_FORCE2")) ctx->force2 = std::atoi(e);
+  if (const char *e = std::getenv("SPH_B200_PIPELINE")) ctx->pipeline = std::atoi(e);
   if (const char *e = std::getenv("SPH_B200_DEN_JS0")) ctx->den_js0 = std::atoi(e);
   if (const char *e = std::getenv("SPH_B200_DEN_JS1")) ctx->den_js1 = std::atoi(e);
   int r = guarded(ctx, [&] {
@@ -1064,15 +1220,29 @@ int sph_step_host(sph_ctx *ctx, void *const *recs, const sph_params *par, double
     CK(cudaEventRecord(e[4], ctx->stream));
     ctx->sweep(SPH_DENSITY, p, path);
     CK(cudaEventRecord(e[5], ctx->stream));
-    ctx->sweep(SPH_FORCE, p, path);
-    CK(cudaEventRecord(e[6], ctx->stream));
-    ctx->sweep(SPH_KICK2, p, path);
-    CK(cudaEventRecord(e[7], ctx->stream));
-    ctx->download_all(recs); // synchronises
-    CK(cudaEventRecord(e[8], ctx->stream));
+    float pl[2] = {0, 0};
+    const bool piped = ctx->can_pipeline(recs);
+    if (piped) {
+      ctx->force_kick2_download_pipelined(recs[0], p, pl);
+      CK(cudaEventRecord(e[6], ctx->stream));
+      CK(cudaEventRecord(e[7], ctx->stream));
+      CK(cudaEventRecord(e[8], ctx->stream));
+    } else {
+      ctx->sweep(SPH_FORCE, p, path);
+      CK(cudaEventRecord(e[6], ctx->stream));
+      ctx->sweep(SPH_KICK2, p, path);
+      CK(cudaEventRecord(e[7], ctx->stream));
+      ctx->download_all(recs); // synchronises
+      CK(cudaEventRecord(e[8], ctx->stream));
+    }
     CK(cudaStreamSynchronize(ctx->stream));
     float ms[8];
     for (int k = 0; k < 8; ++k) CK(cudaEventElapsedTime(&ms[k], e[k], e[k + 1]));
+    if (piped) { // force chunks overlap kick2 and the copy; report the exposed tail as d2h
+      ms[5] = pl[0];
+      ms[6] = 0.0f;
+      ms[7] = pl[1];
+    }
     ctx->stats.last_density_ms = ms[4];
     ctx->stats.last_force_ms = ms[5];
     if (kernel_ms)

@@ -116,6 +116,63 @@ __global__ void compact_kernel(uint4 *__restrict__ dense, const uint4 *__restric
   }
 }
 
+// Host-order records straight from the resident SoA mirror (slots [s0, s1)): every field
+// with a SoA array comes from the SoA, the rest (id, cell, dbg[1], spare) from the AoS
+// record. One thread per 16-byte piece k of a record; the piece layout follows
+// particle.hpp:11-46 (k = offset / 16).
+__global__ void compact_soa_kernel(uint4 *__restrict__ dense, const uint4 *__restrict__ aos,
+                                   SoaMirror f, const int *__restrict__ host_idx, int s0,
+                                   long long total) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
+       i += (long long)gridDim.x * blockDim.x) {
+    const long long r = i / 17;
+    const int k = (int)(i - r * 17);
+    const int s = s0 + (int)r;
+    uint4 v;
+    auto two = [](double a, double b) {
+      return make_uint4(__double2loint(a), __double2hiint(a), __double2loint(b), __double2hiint(b));
+    };
+    switch (k) {
+    case 0: v = two(f.x[s].x, f.x[s].y); break;
+    case 1: v = two(f.v[s].x, f.v[s].y); break;
+    case 2: v = two(f.vp[s].x, f.vp[s].y); break;
+    case 3: v = two(f.a[s].x, f.a[s].y); break;
+    case 4: v = two(f.m[s], f.rho[s]); break;
+    case 5: v = two(f.p[s], f.u[s]); break;
+    case 6: v = two(f.u_pred[s], f.u_dt[s]); break;
+    case 7: v = two(f.c[s], f.h[s]); break;
+    case 8: v = two(f.wcount[s], f.rho_dh[s]); break;
+    case 9: v = two(f.rot_v[s], f.div_v[s]); break;
+    case 10: v = two(f.v_sig[s], f.h_dt[s]); break;
+    case 11: {
+      const double d = f.dt_next[s];
+      v = make_uint4(__double2loint(d), __double2hiint(d), (unsigned)f.frozen[s], (unsigned)f.moved[s]);
+      break;
+    }
+    case 13: {
+      const long long fl = f.flags[s];
+      const double d = f.dbg0[s];
+      v = make_uint4((unsigned)(fl & 0xffffffffLL), (unsigned)((unsigned long long)fl >> 32),
+                     __double2loint(d), __double2hiint(d));
+      break;
+    }
+    default: v = aos[(long long)s * 17 + k]; break; // id/cell, dbg[1], spare
+    }
+    dense[(long long)host_idx[s] * 17 + k] = v;
+  }
+}
+
+// dep[g] = max over slots s in [0, n) with host_idx[s] in host chunk g of the force chunk
+// holding s (chunk f = slots [bounds[f], bounds[f+1]))
+__global__ void host_chunk_dep_kernel(int *dep, const int *__restrict__ host_idx, int n, int hsz,
+                                      ChunkBounds b) {
+  const int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= n) return;
+  int f = 0;
+  while (f + 1 < b.k && s >= b.s[f + 1]) ++f;
+  atomicMax(&dep[host_idx[s] / hsz], f);
+}
+
 __global__ void pack_kernel(char *__restrict__ dense, const Particle *__restrict__ aos,
                             const int *__restrict__ host_idx, int n, uint32_t mask) {
   const int s = blockIdx.x * blockDim.x + threadIdx.x;
@@ -169,13 +226,20 @@ __device__ __forceinline__ int subcell_bin(double2 x, int c, int nx, int ny) {
   return m;
 }
 
-__global__ void spatial_order_kernel(int *__restrict__ ilist, const Particle *__restrict__ aos,
-                                     SoaMirror f, bool aos_src, const int *__restrict__ cell_begin,
-                                     int nx, int ny) {
+// Stable counting sort of each cell's slots by sub-cell bin (one 256-thread CTA per cell):
+// within a bin the slots keep ascending order, so ilist — and with it the FAST summation
+// order — is deterministic run to run.
+__global__ void __launch_bounds__(256) spatial_order_kernel(int *__restrict__ ilist,
+                                                            const Particle *__restrict__ aos,
+                                                            SoaMirror f, bool aos_src,
+                                                            const int *__restrict__ cell_begin,
+                                                            int nx, int ny) {
   __shared__ int hist[64];
   __shared__ int offs[64];
+  __shared__ int wcnt[8][64];
   const int c = blockIdx.x;
   const int b = cell_begin[c], e = cell_begin[c + 1];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   if (threadIdx.x < 64) hist[threadIdx.x] = 0;
   __syncthreads();
   for (int s = b + threadIdx.x; s < e; s += blockDim.x) {
@@ -187,11 +251,31 @@ __global__ void spatial_order_kernel(int *__restrict__ ilist, const Particle *__
     int acc = 0;
     for (int k = 0; k < 64; ++k) { offs[k] = acc; acc += hist[k]; }
   }
+  for (int k = threadIdx.x; k < 8 * 64; k += blockDim.x) (&wcnt[0][0])[k] = 0;
   __syncthreads();
-  for (int s = b + threadIdx.x; s < e; s += blockDim.x) {
-    double2 x = aos_src ? *reinterpret_cast<const double2 *>(aos[s].x) : f.x[s];
-    const int pos = atomicAdd(&offs[subcell_bin(x, c, nx, ny)], 1);
-    ilist[b + pos] = s;
+  for (int s0 = b; s0 < e; s0 += blockDim.x) {
+    const int s = s0 + threadIdx.x;
+    int bin = -1 - lane; // distinct per lane for inactive threads
+    if (s < e) {
+      double2 x = aos_src ? *reinterpret_cast<const double2 *>(aos[s].x) : f.x[s];
+      bin = subcell_bin(x, c, nx, ny);
+    }
+    const unsigned m = __match_any_sync(0xffffffffu, bin);
+    const int rank = __popc(m & ((1u << lane) - 1u));
+    if (s < e && rank == 0) wcnt[w][bin] = __popc(m);
+    __syncthreads();
+    if (s < e) {
+      int pos = offs[bin] + rank;
+      for (int v = 0; v < w; ++v) pos += wcnt[v][bin];
+      ilist[b + pos] = s;
+    }
+    __syncthreads();
+    if (threadIdx.x < 64) {
+      int add = 0;
+      for (int v = 0; v < 8; ++v) { add += wcnt[v][threadIdx.x]; wcnt[v][threadIdx.x] = 0; }
+      offs[threadIdx.x] += add;
+    }
+    __syncthreads();
   }
 }
 
@@ -404,6 +488,18 @@ void launch_compact(Particle *dense, const Particle *aos, const int *host_idx, i
     compact_kernel<<<grid_for(total, 256), 256, 0, s>>>(reinterpret_cast<uint4 *>(dense),
                                                          reinterpret_cast<const uint4 *>(aos),
                                                          host_idx, total);
+}
+void launch_compact_soa(Particle *dense, const Particle *aos, const SoaMirror &f,
+                        const int *host_idx, int s0, int s1, cudaStream_t s) {
+  const long long total = 17LL * (s1 - s0);
+  if (total > 0)
+    compact_soa_kernel<<<grid_for(total, 256), 256, 0, s>>>(reinterpret_cast<uint4 *>(dense),
+                                                             reinterpret_cast<const uint4 *>(aos),
+                                                             f, host_idx, s0, total);
+}
+void launch_host_chunk_dep(int *dep, const int *host_idx, int n, int hsz, const ChunkBounds &b,
+                           cudaStream_t s) {
+  if (n > 0) host_chunk_dep_kernel<<<(n + 255) / 256, 256, 0, s>>>(dep, host_idx, n, hsz, b);
 }
 void launch_pack(char *dense, const Particle *aos, const int *host_idx, int n, uint32_t mask,
                  cudaStream_t s) {

@@ -42,6 +42,17 @@ void launch_scatter(Particle *aos, const SoaMirror &f, int n, uint32_t mask, cud
 // dense (host order) records -> device slots and back (full records)
 void launch_expand(Particle *aos, const Particle *dense, const int *host_idx, int n, cudaStream_t s);
 void launch_compact(Particle *dense, const Particle *aos, const int *host_idx, int n, cudaStream_t s);
+// host-order records of slots [s0, s1) assembled from the resident SoA (+ AoS for the
+// fields without a SoA array)
+void launch_compact_soa(Particle *dense, const Particle *aos, const SoaMirror &f,
+                        const int *host_idx, int s0, int s1, cudaStream_t s);
+// slot ranges of the pipelined force chunks; dep[g] = last chunk touching host chunk g
+struct ChunkBounds {
+  int k;      // chunks
+  int s[17];  // slot bounds, s[0] = 0, s[k] = n
+};
+void launch_host_chunk_dep(int *dep, const int *host_idx, int n, int hsz, const ChunkBounds &b,
+                           cudaStream_t s);
 // pack / unpack selected fields between device slots and a dense per-field buffer in host order.
 // Buffer layout: for each field group in `mask` (ascending bit order) a block of n * size
 // bytes, each block starting 16-byte aligned.
