@@ -533,10 +533,10 @@ struct sph_ctx {
     stats.force_pairs = active_pairs;
   }
 
-  bool can_pipeline(void *const *recs) const {
+  bool can_pipeline(bool contig) const {
     return pipeline && numerics == SPH_NUMERICS_FAST && cull && force2 && !has_owned &&
            mode_for(SPH_PATH_AOS_BASELINE) == SPH_LAYOUT_RESIDENT && nx >= 5 && ny >= 5 &&
-           n >= 4096 && contiguous(recs);
+           n >= 4096 && contig;
   }
 
   // force -> kick2 -> download for host records at `host` (contiguous, bound order), with
@@ -710,19 +710,28 @@ struct sph_ctx {
   }
 
   // ---- host <-> device ----
+  // recs[k] == recs[0] + k * 272 for every k (one flat record array in bound order)
   bool contiguous(void *const *recs) const {
+    if (n <= 0) return true;
     const char *b = static_cast<const char *>(recs[0]);
-    for (int64_t k = 1; k < n; ++k)
-      if (static_cast<const char *>(recs[k]) != b + k * SPH_RECORD_SIZE) return false;
-    return true;
+    std::atomic<bool> ok{true};
+    parallel_for(n, [&](int64_t lo, int64_t hi) {
+      for (int64_t k = lo; k < hi; ++k)
+        if (static_cast<const char *>(recs[k]) != b + k * SPH_RECORD_SIZE) {
+          ok = false;
+          return;
+        }
+    });
+    return ok;
   }
 
   // Full records, bound order -> device slots.
-  void upload_full(void *const *recs) {
+  void upload_full(void *const *recs, int contig = -1) {
     const size_t bytes = (size_t)n * SPH_RECORD_SIZE;
     if (n == 0) return;
     const void *src;
-    if (contiguous(recs)) {
+    if (contig < 0) contig = contiguous(recs);
+    if (contig) {
       src = recs[0];
     } else {
       h_stage.ensure(bytes);
@@ -1210,7 +1219,8 @@ int sph_step_host(sph_ctx *ctx, void *const *recs, const sph_params *par, double
     const int path = SPH_PATH_AOS_BASELINE;
     cudaEvent_t *e = ctx->ev + 6; // ev[6..14]
     CK(cudaEventRecord(e[0], ctx->stream));
-    ctx->upload_full(recs);
+    const bool contig = ctx->contiguous(recs);
+    ctx->upload_full(recs, contig);
     CK(cudaEventRecord(e[1], ctx->stream));
     ctx->sweep(SPH_KICK1, p, path);
     CK(cudaEventRecord(e[2], ctx->stream));
@@ -1221,7 +1231,7 @@ int sph_step_host(sph_ctx *ctx, void *const *recs, const sph_params *par, double
     ctx->sweep(SPH_DENSITY, p, path);
     CK(cudaEventRecord(e[5], ctx->stream));
     float pl[2] = {0, 0};
-    const bool piped = ctx->can_pipeline(recs);
+    const bool piped = ctx->can_pipeline(contig);
     if (piped) {
       ctx->force_kick2_download_pipelined(recs[0], p, pl);
       CK(cudaEventRecord(e[6], ctx->stream));
