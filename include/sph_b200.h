@@ -169,6 +169,34 @@ int sph_synchronize(sph_ctx *ctx);
 /* Measured FP64 FMA throughput of this device (TFLOP/s, 2 flops per DFMA). */
 int sph_fp64_peak(sph_ctx *ctx, double *tflops);
 
+/* ---- Device-resident slab decomposition (paper_2502_16517_b200/decomp.py) ----
+ * The reference has no decomposition; these entry points let one context per GPU hold its
+ * slab's particles on the device while the halo / migration traffic moves between GPUs as
+ * device buffers (NCCL). col_mask is a HOST array of nx bytes selecting cell columns; a
+ * particle's column is build_grid's clamp(floor(x * nx)) (grid.cpp:153) of its current x.
+ * Record / rank / rho buffers are DEVICE pointers. All calls synchronise the context.
+ *   sph_dd_count       particles in the selected columns
+ *   sph_dd_export      copy their records (272 B, current values) and all-ranks out, in slot
+ *                      order (after sph_rebin: (cell, all-rank) order)
+ *   sph_dd_remove      drop them (the remaining slots keep their order)
+ *   sph_dd_append      add m records (+ all-ranks); pair sweeps then need sph_rebin
+ *   sph_dd_export_rho / sph_dd_import_rho
+ *                      rho of the selected particles out / in, in slot order (the halo
+ *                      refresh between density and force: force reads the active
+ *                      particles' rho, kernels.cpp:443-456)
+ * Host-order views (sph_read_records) of a context changed by these calls are in slot
+ * order. */
+int sph_dd_count(sph_ctx *ctx, const uint8_t *col_mask, int64_t *count);
+int sph_dd_export(sph_ctx *ctx, const uint8_t *col_mask, void *dev_recs, int64_t *dev_ranks,
+                  int64_t cap, int64_t *count);
+int sph_dd_remove(sph_ctx *ctx, const uint8_t *col_mask);
+int sph_dd_append(sph_ctx *ctx, const void *dev_recs, const int64_t *dev_ranks, int64_t m);
+int sph_dd_export_rho(sph_ctx *ctx, const uint8_t *col_mask, double *dev_out, int64_t cap,
+                      int64_t *count);
+int sph_dd_import_rho(sph_ctx *ctx, const uint8_t *col_mask, const double *dev_in, int64_t m);
+/* Current particle count of the context. */
+int64_t sph_count(const sph_ctx *ctx);
+
 /* Number of kernel launches issued by this library so far (for bench accounting). */
 int64_t sph_launch_count(const sph_ctx *ctx);
 

@@ -66,6 +66,13 @@ SIGNATURES = {
     "sph_synchronize": (C.c_int, [_vp]),
     "sph_fp64_peak": (C.c_int, [_vp, C.POINTER(C.c_double)]),
     "sph_launch_count": (C.c_int64, [_vp]),
+    "sph_count": (C.c_int64, [_vp]),
+    "sph_dd_count": (C.c_int, [_vp, _vp, C.POINTER(C.c_int64)]),
+    "sph_dd_export": (C.c_int, [_vp, _vp, _vp, _vp, C.c_int64, C.POINTER(C.c_int64)]),
+    "sph_dd_remove": (C.c_int, [_vp, _vp]),
+    "sph_dd_append": (C.c_int, [_vp, _vp, _vp, C.c_int64]),
+    "sph_dd_export_rho": (C.c_int, [_vp, _vp, _vp, C.c_int64, C.POINTER(C.c_int64)]),
+    "sph_dd_import_rho": (C.c_int, [_vp, _vp, _vp, C.c_int64]),
 }
 
 _lib = None

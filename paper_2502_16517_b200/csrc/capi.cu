@@ -225,6 +225,9 @@ struct sph_ctx {
   DevBuf<char> dense, cub_tmp;
   PinnedBuf h_stage, h_small;
   int n_items0 = 0;
+  bool need_rebin = false; // particles were appended: cell lists stale until sph_rebin
+  DevBuf<unsigned char> dd_mask, dd_flag;
+  DevBuf<int> dd_sel, dd_cnt;
   int64_t active_pairs = 0;
 
   // mirror state
@@ -675,8 +678,112 @@ struct sph_ctx {
     return o;
   }
 
+  // ---- domain decomposition (device-resident slabs, decomp.py) ----
+  // Slots whose column clamp(floor(x * nx)) is set in `col_mask` (or clear, `invert`), in
+  // slot order, into dd_sel; returns the count.
+  int64_t dd_select(const uint8_t *col_mask, bool invert) {
+    dd_mask.ensure(nx);
+    CK(cudaMemcpyAsync(dd_mask.p, col_mask, nx, cudaMemcpyHostToDevice, stream));
+    dd_flag.ensure(n);
+    dd_sel.ensure(n);
+    dd_cnt.ensure(1);
+    const bool aos_src = !(soa_ahead || soa_valid);
+    launch_col_flags(dd_flag.p, aos.p, soa, aos_src, dd_mask.p, (int)n, nx, invert ? 1 : 0, stream);
+    size_t tb = 0;
+    cub::CountingInputIterator<int> it(0);
+    CK(cub::DeviceSelect::Flagged(nullptr, tb, it, dd_flag.p, dd_sel.p, dd_cnt.p, (int)n, stream));
+    cub_tmp.ensure(tb);
+    CK(cub::DeviceSelect::Flagged(cub_tmp.p, tb, it, dd_flag.p, dd_sel.p, dd_cnt.p, (int)n, stream));
+    launched(2);
+    int cnt_h = 0;
+    CK(cudaMemcpyAsync(&cnt_h, dd_cnt.p, sizeof(int), cudaMemcpyDeviceToHost, stream));
+    CK(cudaStreamSynchronize(stream));
+    return cnt_h;
+  }
+  int64_t dd_export(const uint8_t *col_mask, Particle *out, long long *ranks_out, int64_t cap) {
+    if (n == 0) return 0;
+    make_aos_current();
+    const int64_t m = dd_select(col_mask, false);
+    if (m > cap) throw ArgError{"export buffer too small"};
+    launch_permute<Particle>(out, aos.p, dd_sel.p, (int)m, stream);
+    if (ranks_out) launch_permute<long long>(ranks_out, all_rank.p, dd_sel.p, (int)m, stream);
+    launched(2);
+    CK(cudaStreamSynchronize(stream));
+    return m;
+  }
+  void dd_reset_host_order() {
+    host_idx.ensure(n);
+    launch_iota(host_idx.p, (int)n, stream);
+    launched();
+    identity_order = true;
+  }
+  void dd_remove(const uint8_t *col_mask) {
+    if (n == 0) return;
+    const int64_t keep = dd_select(col_mask, true);
+    if (keep == n) return;
+    apply_perm(dd_sel.p, keep); // (sel is read before the buffers it indexes are swapped)
+    n = keep;
+    dd_reset_host_order();
+    need_rebin = true;
+    CK(cudaStreamSynchronize(stream));
+  }
+  void dd_append(const Particle *recs, const long long *ranks, int64_t m) {
+    if (m <= 0) return;
+    if (n + m >= (1LL << 31)) throw ArgError{"particle count out of range"};
+    make_aos_current();
+    const int64_t nn = n + m;
+    aos_tmp.ensure(nn);
+    if (n) CK(cudaMemcpyAsync(aos_tmp.p, aos.p, sizeof(Particle) * n, cudaMemcpyDeviceToDevice, stream));
+    CK(cudaMemcpyAsync(aos_tmp.p + n, recs, sizeof(Particle) * m, cudaMemcpyDeviceToDevice, stream));
+    std::swap(aos.p, aos_tmp.p);
+    std::swap(aos.cap, aos_tmp.cap);
+    all_rank_tmp.ensure(nn);
+    if (n) CK(cudaMemcpyAsync(all_rank_tmp.p, all_rank.p, sizeof(long long) * n, cudaMemcpyDeviceToDevice, stream));
+    CK(cudaMemcpyAsync(all_rank_tmp.p + n, ranks, sizeof(long long) * m, cudaMemcpyDeviceToDevice, stream));
+    std::swap(all_rank.p, all_rank_tmp.p);
+    std::swap(all_rank.cap, all_rank_tmp.cap);
+    CK(cudaStreamSynchronize(stream));
+    n = nn;
+    alloc_for(n, ncells); // scratch sized for the new count (aos / all_rank already are)
+    soa_valid = false;    // the SoA is re-gathered from the AoS by the next resident sweep
+    soa_ahead = false;
+    dd_reset_host_order();
+    need_rebin = true;
+    CK(cudaStreamSynchronize(stream));
+  }
+  int64_t dd_export_rho(const uint8_t *col_mask, double *out, int64_t cap) {
+    if (n == 0) return 0;
+    const int64_t m = dd_select(col_mask, false);
+    if (m > cap) throw ArgError{"export buffer too small"};
+    if (soa_ahead || soa_valid) {
+      launch_permute<double>(out, soa.rho, dd_sel.p, (int)m, stream);
+    } else {
+      ensure_soa();
+      launch_gather(aos.p, soa, (int)n, F_RHO, stream);
+      launch_permute<double>(out, soa.rho, dd_sel.p, (int)m, stream);
+    }
+    launched();
+    CK(cudaStreamSynchronize(stream));
+    return m;
+  }
+  void dd_import_rho(const uint8_t *col_mask, const double *in, int64_t m) {
+    if (n == 0 && m == 0) return;
+    make_soa_current();
+    const int64_t k = dd_select(col_mask, false);
+    if (k != m) throw ArgError{"import count does not match the selected particles"};
+    launch_scatter_idx(soa.rho, in, dd_sel.p, (int)m, stream);
+    launched();
+    if (!soa_ahead) { // keep the AoS copy coherent too
+      launch_scatter(aos.p, soa, (int)n, F_RHO, stream);
+      launched();
+    }
+    CK(cudaStreamSynchronize(stream));
+  }
+
   // One sweep on the device. Events: ev[0..3] bracket prologue / compute / epilogue.
   void sweep(int kernel, const Params &par, int path) {
+    if (need_rebin && (kernel == SPH_DENSITY || kernel == SPH_FORCE))
+      throw ArgError{"particles were appended: call sph_rebin before a pair sweep"};
     const int mode = mode_for(path);
     const bool exact = numerics == SPH_NUMERICS_EXACT;
     if (mode == SPH_LAYOUT_RESIDENT) {
@@ -854,8 +961,65 @@ struct sph_ctx {
     stats.active_pairs = active_pairs;
   }
 
+  // Permute every per-particle mirror: new slot k <- old slot perm[k], k < m (m may be
+  // smaller than n: the dropped slots vanish). AoS, host_idx, all_rank, and the SoA arrays
+  // when they hold data.
+  void apply_perm(const int *perm, int64_t m) {
+    aos_tmp.ensure(m);
+    launch_permute<Particle>(aos_tmp.p, aos.p, perm, (int)m, stream);
+    std::swap(aos.p, aos_tmp.p);
+    std::swap(aos.cap, aos_tmp.cap);
+    host_idx_tmp.ensure(m);
+    launch_permute<int>(host_idx_tmp.p, host_idx.p, perm, (int)m, stream);
+    std::swap(host_idx.p, host_idx_tmp.p);
+    std::swap(host_idx.cap, host_idx_tmp.cap);
+    all_rank_tmp.ensure(m);
+    launch_permute<long long>(all_rank_tmp.p, all_rank.p, perm, (int)m, stream);
+    std::swap(all_rank.p, all_rank_tmp.p);
+    std::swap(all_rank.cap, all_rank_tmp.cap);
+    launched(4);
+    if (soa_valid || soa_ahead) {
+      auto p2 = [&](DevBuf<double2> &b) {
+        tmp2.ensure(m);
+        launch_permute<double2>(tmp2.p, b.p, perm, (int)m, stream);
+        std::swap(b.p, tmp2.p);
+        std::swap(b.cap, tmp2.cap);
+        launched();
+      };
+      auto p1 = [&](DevBuf<double> &b) {
+        tmp1.ensure(m);
+        launch_permute<double>(tmp1.p, b.p, perm, (int)m, stream);
+        std::swap(b.p, tmp1.p);
+        std::swap(b.cap, tmp1.cap);
+        launched();
+      };
+      p2(f_x); p2(f_v); p2(f_vp); p2(f_a);
+      p1(f_m); p1(f_rho); p1(f_p); p1(f_u); p1(f_upred); p1(f_udt); p1(f_c); p1(f_h);
+      p1(f_wc); p1(f_rdh); p1(f_rot); p1(f_div); p1(f_vsig); p1(f_hdt); p1(f_dtn); p1(f_dbg0);
+      {
+        // frozen / moved (int32) and flags (int64) through the scratch int / int64 buffers
+        vals.ensure(m);
+        launch_permute<int>(vals.p, f_frozen.p, perm, (int)m, stream);
+        std::swap(f_frozen.p, vals.p);
+        std::swap(f_frozen.cap, vals.cap);
+        launch_permute<int>(vals.p, f_moved.p, perm, (int)m, stream);
+        std::swap(f_moved.p, vals.p);
+        std::swap(f_moved.cap, vals.cap);
+        tmp8.ensure(m);
+        launch_permute<int64_t>(tmp8.p, f_flags.p, perm, (int)m, stream);
+        std::swap(f_flags.p, tmp8.p);
+        std::swap(f_flags.cap, tmp8.cap);
+        launched(3);
+      }
+      soa = SoaMirror{f_x.p, f_v.p, f_vp.p, f_a.p, f_m.p, f_rho.p, f_p.p, f_u.p, f_upred.p,
+                      f_udt.p, f_c.p, f_h.p, f_wc.p, f_rdh.p, f_rot.p, f_div.p, f_vsig.p,
+                      f_hdt.p, f_dtn.p, f_dbg0.p, f_frozen.p, f_moved.p, f_flags.p};
+    }
+  }
+
   void rebin() {
     if (n == 0) return;
+    need_rebin = false;
     const bool soa_src = soa_ahead;
     keys.ensure(n); keys_sorted.ensure(n); vals.ensure(n); vals_sorted.ensure(n); cellnew.ensure(n);
     launch_rebin_keys(keys.p, vals.p, cellnew.p, aos.p, soa, !soa_src, all_rank.p, (int)n, nx, ny, stream);
@@ -871,56 +1035,7 @@ struct sph_ctx {
     launched(4);
     const int *perm = vals_sorted.p;
     launch_cell_begin_from_sorted(cell_begin.p, keys_sorted.p, (int)n, ncells, stream);
-    aos_tmp.ensure(n);
-    launch_permute<Particle>(aos_tmp.p, aos.p, perm, (int)n, stream);
-    std::swap(aos.p, aos_tmp.p);
-    std::swap(aos.cap, aos_tmp.cap);
-    host_idx_tmp.ensure(n);
-    launch_permute<int>(host_idx_tmp.p, host_idx.p, perm, (int)n, stream);
-    std::swap(host_idx.p, host_idx_tmp.p);
-    std::swap(host_idx.cap, host_idx_tmp.cap);
-    all_rank_tmp.ensure(n);
-    launch_permute<long long>(all_rank_tmp.p, all_rank.p, perm, (int)n, stream);
-    std::swap(all_rank.p, all_rank_tmp.p);
-    std::swap(all_rank.cap, all_rank_tmp.cap);
-    launched(4);
-    if (soa_valid || soa_ahead) {
-      auto p2 = [&](DevBuf<double2> &b) {
-        tmp2.ensure(n);
-        launch_permute<double2>(tmp2.p, b.p, perm, (int)n, stream);
-        std::swap(b.p, tmp2.p);
-        std::swap(b.cap, tmp2.cap);
-        launched();
-      };
-      auto p1 = [&](DevBuf<double> &b) {
-        tmp1.ensure(n);
-        launch_permute<double>(tmp1.p, b.p, perm, (int)n, stream);
-        std::swap(b.p, tmp1.p);
-        std::swap(b.cap, tmp1.cap);
-        launched();
-      };
-      p2(f_x); p2(f_v); p2(f_vp); p2(f_a);
-      p1(f_m); p1(f_rho); p1(f_p); p1(f_u); p1(f_upred); p1(f_udt); p1(f_c); p1(f_h);
-      p1(f_wc); p1(f_rdh); p1(f_rot); p1(f_div); p1(f_vsig); p1(f_hdt); p1(f_dtn); p1(f_dbg0);
-      {
-        // frozen / moved (int32) and flags (int64) through the scratch int / int64 buffers
-        vals.ensure(n);
-        launch_permute<int>(vals.p, f_frozen.p, perm, (int)n, stream);
-        std::swap(f_frozen.p, vals.p);
-        std::swap(f_frozen.cap, vals.cap);
-        launch_permute<int>(vals.p, f_moved.p, perm, (int)n, stream);
-        std::swap(f_moved.p, vals.p);
-        std::swap(f_moved.cap, vals.cap);
-        tmp8.ensure(n);
-        launch_permute<int64_t>(tmp8.p, f_flags.p, perm, (int)n, stream);
-        std::swap(f_flags.p, tmp8.p);
-        std::swap(f_flags.cap, tmp8.cap);
-        launched(3);
-      }
-      soa = SoaMirror{f_x.p, f_v.p, f_vp.p, f_a.p, f_m.p, f_rho.p, f_p.p, f_u.p, f_upred.p,
-                      f_udt.p, f_c.p, f_h.p, f_wc.p, f_rdh.p, f_rot.p, f_div.p, f_vsig.p,
-                      f_hdt.p, f_dtn.p, f_dbg0.p, f_frozen.p, f_moved.p, f_flags.p};
-    }
+    apply_perm(perm, n);
     launch_set_cell(aos.p, cell_begin.p, ncells, stream); // build_grid writes p->cell (grid.cpp:156)
     launched();
     dirty |= F_CELL;
@@ -1409,5 +1524,74 @@ int sph_fp64_peak(sph_ctx *ctx, double *tflops) {
 }
 
 int64_t sph_launch_count(const sph_ctx *ctx) { return ctx ? ctx->launches : 0; }
+
+int64_t sph_count(const sph_ctx *ctx) { return ctx ? ctx->n : 0; }
+
+namespace {
+void dd_check(sph_ctx *ctx, const void *mask) {
+  if (!ctx->bound) throw ArgError{"decomposition call before sph_bind"};
+  if (!mask) throw ArgError{"null column mask"};
+}
+} // namespace
+
+int sph_dd_count(sph_ctx *ctx, const uint8_t *col_mask, int64_t *count) {
+  return guarded(ctx, [&] {
+    dd_check(ctx, col_mask);
+    const int64_t m = ctx->n ? ctx->dd_select(col_mask, false) : 0;
+    if (count) *count = m;
+    return SPH_OK;
+  });
+}
+
+int sph_dd_export(sph_ctx *ctx, const uint8_t *col_mask, void *dev_recs, int64_t *dev_ranks,
+                  int64_t cap, int64_t *count) {
+  return guarded(ctx, [&] {
+    dd_check(ctx, col_mask);
+    if (!dev_recs && cap > 0) throw ArgError{"null record buffer"};
+    const int64_t m = ctx->dd_export(col_mask, static_cast<Particle *>(dev_recs),
+                                     reinterpret_cast<long long *>(dev_ranks), cap);
+    if (count) *count = m;
+    return SPH_OK;
+  });
+}
+
+int sph_dd_remove(sph_ctx *ctx, const uint8_t *col_mask) {
+  return guarded(ctx, [&] {
+    dd_check(ctx, col_mask);
+    ctx->dd_remove(col_mask);
+    ctx->stats.n = ctx->n;
+    return SPH_OK;
+  });
+}
+
+int sph_dd_append(sph_ctx *ctx, const void *dev_recs, const int64_t *dev_ranks, int64_t m) {
+  return guarded(ctx, [&] {
+    if (!ctx->bound) throw ArgError{"decomposition call before sph_bind"};
+    if (m < 0 || (m > 0 && (!dev_recs || !dev_ranks))) throw ArgError{"bad append"};
+    ctx->dd_append(static_cast<const Particle *>(dev_recs),
+                   reinterpret_cast<const long long *>(dev_ranks), m);
+    ctx->stats.n = ctx->n;
+    return SPH_OK;
+  });
+}
+
+int sph_dd_export_rho(sph_ctx *ctx, const uint8_t *col_mask, double *dev_out, int64_t cap,
+                      int64_t *count) {
+  return guarded(ctx, [&] {
+    dd_check(ctx, col_mask);
+    const int64_t m = ctx->dd_export_rho(col_mask, dev_out, cap);
+    if (count) *count = m;
+    return SPH_OK;
+  });
+}
+
+int sph_dd_import_rho(sph_ctx *ctx, const uint8_t *col_mask, const double *dev_in, int64_t m) {
+  return guarded(ctx, [&] {
+    dd_check(ctx, col_mask);
+    if (m > 0 && !dev_in) throw ArgError{"null rho buffer"};
+    ctx->dd_import_rho(col_mask, dev_in, m);
+    return SPH_OK;
+  });
+}
 
 } // extern "C"

@@ -489,6 +489,39 @@ void launch_compact(Particle *dense, const Particle *aos, const int *host_idx, i
                                                          reinterpret_cast<const uint4 *>(aos),
                                                          host_idx, total);
 }
+// ---- domain decomposition helpers ----
+// flag[s] = col_mask[column of slot s] ^ invert, column = clamp(floor(x * nx)) (grid.cpp:153)
+__global__ void col_flags_kernel(unsigned char *__restrict__ flag, const Particle *__restrict__ aos,
+                                 SoaMirror f, bool aos_src, const unsigned char *__restrict__ mask,
+                                 int n, int nx, int invert) {
+  const int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= n) return;
+  const double x = aos_src ? aos[s].x[0] : f.x[s].x;
+  int cx = (int)floor(x * nx);
+  cx = min(nx - 1, max(0, cx));
+  flag[s] = (unsigned char)((mask[cx] != 0) ^ (invert != 0));
+}
+__global__ void iota_kernel(int *__restrict__ v, int n) {
+  const int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s < n) v[s] = s;
+}
+__global__ void scatter_idx_kernel(double *__restrict__ dst, const double *__restrict__ src,
+                                   const int *__restrict__ idx, int m) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k < m) dst[idx[k]] = src[k];
+}
+
+void launch_col_flags(unsigned char *flag, const Particle *aos, const SoaMirror &f, bool aos_src,
+                      const unsigned char *mask, int n, int nx, int invert, cudaStream_t s) {
+  if (n > 0) col_flags_kernel<<<(n + 255) / 256, 256, 0, s>>>(flag, aos, f, aos_src, mask, n, nx, invert);
+}
+void launch_iota(int *v, int n, cudaStream_t s) {
+  if (n > 0) iota_kernel<<<(n + 255) / 256, 256, 0, s>>>(v, n);
+}
+void launch_scatter_idx(double *dst, const double *src, const int *idx, int m, cudaStream_t s) {
+  if (m > 0) scatter_idx_kernel<<<(m + 255) / 256, 256, 0, s>>>(dst, src, idx, m);
+}
+
 void launch_compact_soa(Particle *dense, const Particle *aos, const SoaMirror &f,
                         const int *host_idx, int s0, int s1, cudaStream_t s) {
   const long long total = 17LL * (s1 - s0);

@@ -46,6 +46,11 @@ void launch_compact(Particle *dense, const Particle *aos, const int *host_idx, i
 // fields without a SoA array)
 void launch_compact_soa(Particle *dense, const Particle *aos, const SoaMirror &f,
                         const int *host_idx, int s0, int s1, cudaStream_t s);
+// domain decomposition: column-mask flags per slot, iota, indexed scatter
+void launch_col_flags(unsigned char *flag, const Particle *aos, const SoaMirror &f, bool aos_src,
+                      const unsigned char *mask, int n, int nx, int invert, cudaStream_t s);
+void launch_iota(int *v, int n, cudaStream_t s);
+void launch_scatter_idx(double *dst, const double *src, const int *idx, int m, cudaStream_t s);
 // slot ranges of the pipelined force chunks; dep[g] = last chunk touching host chunk g
 struct ChunkBounds {
   int k;      // chunks

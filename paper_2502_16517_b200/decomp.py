@@ -258,3 +258,164 @@ class DistributedSim:
         recs = np.concatenate([o[0] for o in objs])
         ranks = np.concatenate([o[1] for o in objs])
         return recs[np.argsort(ranks)]
+
+
+class DeviceSlabSim:
+    """One rank of the DEVICE-RESIDENT slab decomposition (BASELINE config 5).
+
+    The rank's context holds its slab's particles on its GPU for the whole run. Per step:
+    kick1 + drift -> migration (records of particles whose column left the slab go to the
+    neighbour that owns it) -> halo (records of my boundary columns to each neighbour,
+    appended as halo particles) -> device rebin -> density on owned cells -> rho refresh of
+    the halo (force reads the active particles' rho, kernels.cpp:443-456) -> force on owned
+    cells -> kick2 -> drop the halo. Every transfer is a device buffer exported / imported
+    by the C-ABI (sph_dd_*) and moved with ``torch.distributed`` point-to-point ops: NCCL
+    over NVLink between GPUs; with the gloo backend (CPU tests, ranks sharing one GPU) the
+    buffers are staged through host memory. Owned cells see exactly the reference's active
+    lists (halo particles keep their global cell and all-rank), so k ranks reproduce one
+    rank byte for byte.
+    """
+
+    def __init__(self, ctx, decomp: SlabDecomposition, group=None):
+        import torch
+        self.ctx, self.d, self.group = ctx, decomp, group
+        self.torch = torch
+        self.dev = torch.device("cuda", torch.cuda.current_device())
+        self.nccl = False
+        if decomp.world > 1:
+            import torch.distributed as dist
+            self.dist = dist
+            self.nccl = dist.get_backend(group) == "nccl"
+        nx = decomp.nx
+        self.mine = np.zeros(nx, np.uint8)
+        self.mine[decomp.owned_cols()] = 1
+        self.not_mine = (1 - self.mine).astype(np.uint8)
+        self.peers = decomp.neighbours()
+        self.cols_of = {}   # columns owned by peer q (migration destinations)
+        self.send_to = {}   # my columns in q's halo
+        self.halo_from = {}  # my halo columns owned by q
+        for q in self.peers:
+            m = np.zeros(nx, np.uint8)
+            m[decomp.owned_cols(q)] = 1
+            self.cols_of[q] = m
+            s = np.zeros(nx, np.uint8)
+            s[decomp.send_cols(q)] = 1
+            self.send_to[q] = s
+            h = np.zeros(nx, np.uint8)
+            h[np.intersect1d(decomp.halo_cols(), decomp.owned_cols(q))] = 1
+            self.halo_from[q] = h
+        self.bytes_sent = 0
+
+    @staticmethod
+    def start(ctx, decomp: SlabDecomposition) -> None:
+        """Keep this rank's columns of a globally bound context and set the owned cells."""
+        mine = np.zeros(decomp.nx, np.uint8)
+        mine[decomp.owned_cols()] = 1
+        if decomp.world > 1:
+            ctx.dd_remove(1 - mine)
+            ctx.rebin()
+        ctx.set_owned_cells(decomp.owned_cells_mask().astype(np.uint8))
+
+    # ---- transport ----
+    def _exchange(self, sends: dict):
+        """sends[q] = tuple of 1-D device tensors; returns the peers' tuples (same dtypes)."""
+        torch, dist = self.torch, self.dist
+        stage = (lambda t: t) if self.nccl else (lambda t: t.cpu())
+        home = self.dev if self.nccl else torch.device("cpu")
+        first = next(iter(sends.values()))
+        # counts first (element counts of every tensor in the tuple)
+        cnt_out = {q: torch.tensor([t.numel() for t in sends[q]], dtype=torch.int64, device=home)
+                   for q in self.peers}
+        cnt_in = {q: torch.zeros(len(first), dtype=torch.int64, device=home) for q in self.peers}
+        ops = []
+        for q in self.peers:
+            ops.append(dist.P2POp(dist.isend, cnt_out[q], q, group=self.group))
+            ops.append(dist.P2POp(dist.irecv, cnt_in[q], q, group=self.group))
+        for r in dist.batch_isend_irecv(ops):
+            r.wait()
+        ops, recv, keep = [], {}, []
+        for q in self.peers:
+            bufs = []
+            for t, m in zip(sends[q], cnt_in[q].tolist()):
+                if t.numel():
+                    st = stage(t)
+                    keep.append(st)
+                    ops.append(dist.P2POp(dist.isend, st, q, group=self.group))
+                    self.bytes_sent += st.numel() * st.element_size()
+                b = torch.empty(int(m), dtype=t.dtype, device=home)
+                if m:
+                    ops.append(dist.P2POp(dist.irecv, b, q, group=self.group))
+                bufs.append(b)
+            recv[q] = bufs
+        if ops:
+            for r in dist.batch_isend_irecv(ops):
+                r.wait()
+        return {q: tuple(b.to(self.dev) for b in recv[q]) for q in self.peers}
+
+    def _export(self, mask):
+        torch = self.torch
+        m = self.ctx.dd_count(mask)
+        recs = torch.empty(max(m, 1) * RECORD_SIZE, dtype=torch.uint8, device=self.dev)
+        ranks = torch.empty(max(m, 1), dtype=torch.int64, device=self.dev)
+        torch.cuda.synchronize()
+        got = self.ctx.dd_export(mask, recs.data_ptr(), ranks.data_ptr(), m)
+        assert got == m
+        return recs[: m * RECORD_SIZE], ranks[:m]
+
+    def _append(self, recs, ranks):
+        m = ranks.numel()
+        if m:
+            self.torch.cuda.synchronize()
+            self.ctx.dd_append(recs.data_ptr(), ranks.data_ptr(), m)
+
+    # ---- the step ----
+    def step(self, par: SphParams) -> None:
+        ctx, d = self.ctx, self.d
+        ctx.sweep(KernelId.Kick1, par)
+        ctx.sweep(KernelId.Drift, par)
+        if d.world > 1:
+            # migration: particles whose column left the slab go to its owner
+            leaving = ctx.dd_count(self.not_mine)
+            sends = {q: self._export(self.cols_of[q]) for q in self.peers}
+            if sum(int(s[1].numel()) for s in sends.values()) != leaving:
+                raise RuntimeError("a particle moved more than one slab in one step")
+            got = self._exchange(sends)
+            ctx.dd_remove(self.not_mine)
+            for q in self.peers:
+                self._append(*got[q])
+            # halo: my boundary columns to each neighbour
+            got = self._exchange({q: self._export(self.send_to[q]) for q in self.peers})
+            for q in self.peers:
+                self._append(*got[q])
+        ctx.rebin()
+        ctx.sweep(KernelId.Density, par)
+        if d.world > 1:
+            torch = self.torch
+            sends = {}
+            for q in self.peers:
+                m = ctx.dd_count(self.send_to[q])
+                buf = torch.empty(max(m, 1), dtype=torch.float64, device=self.dev)
+                torch.cuda.synchronize()
+                ctx.dd_export_rho(self.send_to[q], buf.data_ptr(), m)
+                sends[q] = (buf[:m],)
+            got = self._exchange(sends)
+            torch.cuda.synchronize()
+            for q in self.peers:
+                ctx.dd_import_rho(self.halo_from[q], got[q][0].data_ptr(), got[q][0].numel())
+        ctx.sweep(KernelId.Force, par)
+        ctx.sweep(KernelId.Kick2, par)
+        if d.world > 1:
+            ctx.dd_remove(self.not_mine)  # drop the halo
+
+    def gather_sorted(self):
+        """All owned records of every rank in all-rank order (tests)."""
+        torch = self.torch
+        recs, ranks = self._export(np.ones(self.d.nx, np.uint8))
+        r = recs.cpu().numpy().view(PARTICLE_DTYPE)
+        k = ranks.cpu().numpy()
+        if self.d.world > 1:
+            objs = [None] * self.d.world
+            self.dist.all_gather_object(objs, (r, k), group=self.group)
+            r = np.concatenate([o[0] for o in objs])
+            k = np.concatenate([o[1] for o in objs])
+        return r[np.argsort(k, kind="stable")], np.sort(k)

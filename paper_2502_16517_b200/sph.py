@@ -259,6 +259,58 @@ class Context:
         self._ptrs = grid.record_pointers()
         return store, grid, SphParams(cp.dt, cp.gamma, cp.cfl, cp.grav, cp.target_wcount)
 
+    def make_particles_device(self, n: int, ppc: int, seed: int, kind: int = 0) -> SphParams:
+        """make_particles bound on the device only (no host copy of the records): the
+        starting point of a decomposed run, which then drops the other ranks' columns."""
+        cp = _lib.SphParamsC()
+        _check(self.h, self.lib.sph_make_particles_ex(self.h, n, ppc, seed, int(kind),
+                                                      C.byref(cp)), "sph_make_particles_ex")
+        self.grid = "device"  # bound, no host store
+        self._ptrs = None
+        return SphParams(cp.dt, cp.gamma, cp.cfl, cp.grav, cp.target_wcount)
+
+    # -- device-resident slab decomposition (sph_dd_*; pointers are device addresses) --
+    def count(self) -> int:
+        return int(self.lib.sph_count(self.h))
+
+    def dd_count(self, col_mask: np.ndarray) -> int:
+        m = np.ascontiguousarray(col_mask, np.uint8)
+        out = C.c_int64()
+        _check(self.h, self.lib.sph_dd_count(self.h, m.ctypes.data, C.byref(out)), "sph_dd_count")
+        return out.value
+
+    def dd_export(self, col_mask: np.ndarray, recs_ptr: int, ranks_ptr: int, cap: int) -> int:
+        m = np.ascontiguousarray(col_mask, np.uint8)
+        out = C.c_int64()
+        _check(self.h, self.lib.sph_dd_export(self.h, m.ctypes.data, recs_ptr, ranks_ptr, cap,
+                                              C.byref(out)), "sph_dd_export")
+        return out.value
+
+    def dd_remove(self, col_mask: np.ndarray) -> None:
+        m = np.ascontiguousarray(col_mask, np.uint8)
+        _check(self.h, self.lib.sph_dd_remove(self.h, m.ctypes.data), "sph_dd_remove")
+
+    def dd_append(self, recs_ptr: int, ranks_ptr: int, count: int) -> None:
+        _check(self.h, self.lib.sph_dd_append(self.h, recs_ptr, ranks_ptr, count), "sph_dd_append")
+
+    def dd_export_rho(self, col_mask: np.ndarray, out_ptr: int, cap: int) -> int:
+        m = np.ascontiguousarray(col_mask, np.uint8)
+        out = C.c_int64()
+        _check(self.h, self.lib.sph_dd_export_rho(self.h, m.ctypes.data, out_ptr, cap,
+                                                  C.byref(out)), "sph_dd_export_rho")
+        return out.value
+
+    def dd_import_rho(self, col_mask: np.ndarray, in_ptr: int, count: int) -> None:
+        m = np.ascontiguousarray(col_mask, np.uint8)
+        _check(self.h, self.lib.sph_dd_import_rho(self.h, m.ctypes.data, in_ptr, count),
+               "sph_dd_import_rho")
+
+    def read_records_all(self) -> np.ndarray:
+        """Every record of the context in slot order (device-only contexts included)."""
+        out = np.zeros(max(self.count(), 1), PARTICLE_DTYPE)
+        _check(self.h, self.lib.sph_read_records(self.h, out.ctypes.data), "sph_read_records")
+        return out[: self.count()]
+
     def read_records(self) -> np.ndarray:
         self._need()
         out = np.zeros(len(self._ptrs), PARTICLE_DTYPE)
