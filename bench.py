@@ -20,8 +20,9 @@ SPH steps/s is reported beside it.
            a bounded sample of cells scaled by pair count (oracle/ref_bench.py)
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-N>1 (torchrun): weak scaling, one independent full-size replica per GPU (the pair
-sweeps have no cross-replica exchange); time = max over ranks.
+N>1 (torchrun): weak scaling, --particles per GPU of one global box slab-decomposed
+over the GPUs (device-resident slabs, NCCL migration / halo / rho exchange each step,
+decomp.DeviceSlabSim); time = device events around the K steps, max over ranks.
 """
 from __future__ import annotations
 
@@ -71,7 +72,7 @@ def load_traffic():
     try:
         with open(p) as f:
             d = json.load(f)
-        k = d["kernels"]["force_kernel<FastPolicy>"]
+        k = d["kernels"].get("force2_kernel") or d["kernels"]["force_kernel<FastPolicy>"]
         return k["dram_bytes_read"] + k["dram_bytes_write"], d.get("source", p)
     except Exception:
         return None, None
@@ -143,8 +144,15 @@ def dist_init():
     if world > 1:
         import torch
         import torch.distributed as dist
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if os.environ.get("SPH_BENCH_SHARE_GPU") == "1":
+            # functional check of the N>1 path on a one-GPU box: every rank on GPU 0, gloo
+            # (host-staged) exchanges; the timings of such a run mean nothing
+            local = 0
+            torch.cuda.set_device(0)
+            dist.init_process_group("gloo")
+        else:
+            torch.cuda.set_device(local)
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     return rank, world, local
 
 
@@ -186,7 +194,130 @@ def config_block(args, grid, world):
             "parallelism": f"replicas x{world}" if world > 1 else "single GPU"}
 
 
+def grid_nx(n, ppc):
+    """grid.cpp:23-26."""
+    import math
+    return max(1, int(math.floor(1.0 / math.sqrt(ppc / max(n, 1)))))
+
+
+def run_decomposed(args, rank, world, local):
+    """N > 1 GPUs: weak scaling. One global box of N * args.n particles (the reference IC,
+    nx = floor(sqrt(N n / ppc))) is cut into N slabs of cell columns; each GPU keeps its
+    slab on the device and exchanges migration records, halo records and the halo rho
+    refresh with its two neighbours over NCCL every step (decomp.DeviceSlabSim). Time:
+    device events around K steps, max over ranks."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_2502_16517_b200 as pkg
+    from paper_2502_16517_b200 import DeviceLayout, Numerics
+    from paper_2502_16517_b200.decomp import DeviceSlabSim, SlabDecomposition
+
+    ctx = pkg.Context(local, numerics=Numerics[args.numerics.capitalize()],
+                      layout=DeviceLayout.Resident)
+    n_glob = args.n * world
+    t0 = time.time()
+    par = ctx.make_particles_device(n_glob, args.ppc, args.seed, kind=IC_KIND[args.ic])
+    par.dt = args.dt
+    nx = grid_nx(n_glob, args.ppc)
+    d = SlabDecomposition(nx, nx, world, rank)
+    DeviceSlabSim.start(ctx, d)
+    sim = DeviceSlabSim(ctx, d)
+    t_ic = time.time() - t0
+    dev = torch.device("cuda", local)
+
+    def total(v, op=dist.ReduceOp.SUM):
+        t = torch.tensor([float(v)], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=op)
+        return float(t.item())
+
+    for _ in range(args.warmup):
+        sim.step(par)
+    workload_pairs = total(2 * ctx.stats()["active_pairs"])
+    n_local = ctx.count()
+    torch.cuda.synchronize()
+    dist.barrier()
+    launches0 = ctx.launch_count()
+    sent0 = sim.bytes_sent
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    den = forc = 0.0
+    with ClockSampler(local) as clk:
+        e0.record()
+        for _ in range(args.steps):
+            sim.step(par)
+            st = ctx.stats()
+            den += st["last_density_ms"]
+            forc += st["last_force_ms"]
+        e1.record()
+        torch.cuda.synchronize()
+    dist.barrier()
+    ms_total = total(e0.elapsed_time(e1), dist.ReduceOp.MAX)
+    ms_per_step = ms_total / args.steps
+    launches = ctx.launch_count() - launches0
+    out = {
+        "metric": METRIC, "value": workload_pairs / (ms_per_step * 1e-3), "unit": UNIT,
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic: reference make_particles IC of the global box (uniform random 2-D, "
+                "seed 42), generated on each device, byte-identical to the reference",
+        "config": {"workload": f"full SPH step, {args.n} particles per GPU, global box of "
+                               f"{n_glob} particles (nx={nx}), ppc={args.ppc}, slab decomposition",
+                   "ic": args.ic, "n": n_glob, "n_per_gpu": args.n, "ppc": args.ppc, "nx": nx,
+                   "seed": args.seed, "dt": args.dt, "numerics": args.numerics,
+                   "layout": "resident",
+                   "l2": "inputs larger than L2 (>= 1 GB of mirrors per GPU)",
+                   "parallelism": f"slab decomposition x{world} (NCCL halo + migration)"},
+        "steps_per_s": 1e3 / ms_per_step,
+        "workload_pairs_per_step": workload_pairs,
+        "phase_ms": {"density": den / args.steps, "force": forc / args.steps},
+        "exchange_bytes_per_step_rank0": (sim.bytes_sent - sent0) / args.steps,
+        "ic_seconds": round(t_ic, 2),
+        "gpu_launches": launches,
+        "gpu_launches_per_step": launches / args.steps,
+        "clocks": clk.summary(),
+    }
+    # e2e: the rank's owned records come from pinned host memory before every step and go
+    # back after it (sph_dd_append / sph_dd_export through the C-ABI)
+    if args.e2e_steps > 0:
+        allm = np.ones(nx, np.uint8)
+        host = torch.empty(n_local * 272 + 4096, dtype=torch.uint8, pin_memory=True)
+        hrank = torch.empty(n_local + 16, dtype=torch.int64, pin_memory=True)
+        wall = []
+        for it in range(args.e2e_steps + 1):
+            dist.barrier()
+            t1 = time.perf_counter()
+            if it > 0:  # host -> device: replace the device state with the host records
+                m = hrank_n
+                recs_d = host[: m * 272].to(dev, non_blocking=True)
+                ranks_d = hrank[:m].to(dev, non_blocking=True)
+                torch.cuda.synchronize()
+                ctx.dd_remove(allm)
+                ctx.dd_append(recs_d.data_ptr(), ranks_d.data_ptr(), m)
+            sim.step(par)
+            recs_d, ranks_d = sim._export(allm)  # device -> host: the step's result
+            hrank_n = ranks_d.numel()
+            if hrank_n * 272 > host.numel():
+                host = torch.empty(hrank_n * 272 + 4096, dtype=torch.uint8, pin_memory=True)
+                hrank = torch.empty(hrank_n + 16, dtype=torch.int64, pin_memory=True)
+            host[: hrank_n * 272].copy_(recs_d)
+            hrank[:hrank_n].copy_(ranks_d)
+            torch.cuda.synchronize()
+            if it > 0:
+                wall.append(time.perf_counter() - t1)
+        e2e_s = total(float(np.mean(wall)), dist.ReduceOp.MAX)
+        nb = total(n_local * 272, dist.ReduceOp.MAX)
+        out["e2e"] = {"value": workload_pairs / e2e_s, "unit": UNIT,
+                      "h2d_bytes_per_step": int(nb), "d2h_bytes_per_step": int(nb),
+                      "ms_per_step": e2e_s * 1e3, "steps": args.e2e_steps,
+                      "api": "per rank: H2D of the owned records (sph_dd_append), the "
+                             "decomposed step, D2H of the owned records (sph_dd_export)"}
+    ctx.close()
+    return out if rank == 0 else None
+
+
 def run_ours(args, rank, world, local):
+    if world > 1:
+        return run_decomposed(args, rank, world, local)
     import paper_2502_16517_b200 as pkg
     from paper_2502_16517_b200 import DeviceLayout, Numerics
 
@@ -287,7 +418,7 @@ def _finish(out, ctx, store, grid, par, args, rank, world, ph, names, den_eval, 
         ach_d = dfl * (den_eval / args.steps) / (ph[3] * 1e-3) / 1e12
         traffic, tsrc = load_traffic()
         out["roofline"] = {
-            "bound": "fp64", "kernel": "force_kernel<FastPolicy>", "achieved": ach_f,
+            "bound": "fp64", "kernel": "force2_kernel", "achieved": ach_f,
             "peak": fp64, "unit": "TFLOP/s", "frac": ach_f / fp64, "traffic": traffic,
             "traffic_source": tsrc,
             "flops_per_pair": ffl, "pairs_per_launch": fpairs, "launch_ms": ph[4],
@@ -379,7 +510,8 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--n", type=int, default=1 << 21)
+    ap.add_argument("--particles", dest="n", type=int, default=1 << 21,
+                    help="particles (per GPU when --gpus > 1)")
     ap.add_argument("--ppc", type=int, default=1024)
     ap.add_argument("--seed", type=int, default=42)
     ap.add_argument("--dt", type=float, default=1e-4)
