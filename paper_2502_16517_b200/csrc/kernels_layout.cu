@@ -167,10 +167,16 @@ __global__ void compact_soa_kernel(uint4 *__restrict__ dense, const uint4 *__res
 __global__ void host_chunk_dep_kernel(int *dep, const int *__restrict__ host_idx, int n, int hsz,
                                       ChunkBounds b) {
   const int s = blockIdx.x * blockDim.x + threadIdx.x;
-  if (s >= n) return;
-  int f = 0;
-  while (f + 1 < b.k && s >= b.s[f + 1]) ++f;
-  atomicMax(&dep[host_idx[s] / hsz], f);
+  const bool live = s < n;
+  int f = 0, g = -1 - (int)(threadIdx.x & 31);
+  if (live) {
+    while (f + 1 < b.k && s >= b.s[f + 1]) ++f;
+    g = host_idx[s] / hsz;
+  }
+  // host order is close to slot order: lanes mostly share g, so one atomic per group
+  const unsigned grp = __match_any_sync(0xffffffffu, g);
+  const int fm = __reduce_max_sync(grp, f);
+  if (live && (threadIdx.x & 31) == __ffs(grp) - 1) atomicMax(&dep[g], fm);
 }
 
 __global__ void pack_kernel(char *__restrict__ dense, const Particle *__restrict__ aos,
