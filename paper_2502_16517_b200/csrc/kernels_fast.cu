@@ -427,9 +427,20 @@ __device__ __forceinline__ int spline_row(double q) {
   return (hq < 0x3FE00000 ? 1 : 0) + (hq < 0x3FF80000 ? 1 : 0);
 }
 
-#ifndef SPH_MINB_F2
-#define SPH_MINB_F2 5
+// force2 / density2 CTA shape: W warps per CTA, MINB CTAs per SM requested from ptxas
+// (registers <= 65536 / (32 W MINB)). Measured at 2^21 / ppc 1024 (ms, force / density
+// round 0): 4 warps x 5 (96 regs) 33.31 / 19.07; 1 x 20 (96) 33.11 / 18.74; 1 x 16 (115)
+// 33.48 / 19.68; 1 x 22 or 24 and 2 x 11 (80 regs, spills) 35.8-36.1 / 19.7-19.8.
+#ifndef SPH_F2_WPC
+#define SPH_F2_WPC 1
 #endif
+#ifndef SPH_MINB_F2
+#define SPH_MINB_F2 20
+#endif
+#ifndef SPH_D2_WPC
+#define SPH_D2_WPC 1
+#endif
+constexpr int kF2W = SPH_F2_WPC, kD2W = SPH_D2_WPC;
 
 // SPH part of force_pair (kernels.cpp:132-152) for one in-support pair: accumulates u_dt,
 // h_dt, v_sig and returns the SPH radial factor A*g (the caller applies K).
@@ -502,11 +513,11 @@ __device__ __forceinline__ void force2_stage(F2Tile &T, const ActiveLayout &L, c
 }
 
 template <int MINB>
-__global__ void __launch_bounds__(kWarpsPerCta * 32, MINB) force2_kernel(F2Args A) {
-  __shared__ F2Tile tiles[kWarpsPerCta][2];
-  __shared__ ActiveLayout lay[kWarpsPerCta];
+__global__ void __launch_bounds__(kF2W * 32, MINB) force2_kernel(F2Args A) {
+  __shared__ F2Tile tiles[kF2W][2];
+  __shared__ ActiveLayout lay[kF2W];
   const int w = warp_in_cta(), lane = lane_id();
-  const int item_idx = blockIdx.x * kWarpsPerCta + w;
+  const int item_idx = blockIdx.x * kF2W + w;
   if (item_idx >= A.n_items) return;
   if (lane < 9) tiles[w][0].spl[lane] = tiles[w][1].spl[lane] = kSplE[lane];
   ActiveLayout &L = lay[w];
@@ -710,7 +721,7 @@ __device__ __forceinline__ void density2_pair(const FastPolicy::DI &I, const D2T
 }
 
 #ifndef SPH_MINB_D2
-#define SPH_MINB_D2 5
+#define SPH_MINB_D2 20 // with SPH_D2_WPC = 1: 20 one-warp CTAs per SM, <= 96 registers
 #endif
 
 // JS lanes share one local particle i (j-slices): the warp holds 32/JS particles, which
@@ -719,11 +730,11 @@ __device__ __forceinline__ void density2_pair(const FastPolicy::DI &I, const D2T
 // tight as in round 0. Lane slice q takes j = q, q + JS, ... of each tile; the JS partial
 // sums are combined with shuffles at the end.
 template <int MINB, int JS>
-__global__ void __launch_bounds__(kWarpsPerCta * 32, MINB) density2_kernel(DenArgs A) {
-  __shared__ D2Tile tiles[kWarpsPerCta][2];
-  __shared__ ActiveLayout lay[kWarpsPerCta];
+__global__ void __launch_bounds__(kD2W * 32, MINB) density2_kernel(DenArgs A) {
+  __shared__ D2Tile tiles[kD2W][2];
+  __shared__ ActiveLayout lay[kD2W];
   const int w = warp_in_cta(), lane = lane_id();
-  const int item_idx = blockIdx.x * kWarpsPerCta + w;
+  const int item_idx = blockIdx.x * kD2W + w;
   if (item_idx >= A.n_items) return;
   if (lane < 18) tiles[w][0].spl[lane] = tiles[w][1].spl[lane] = kSplPE[lane];
   ActiveLayout &L = lay[w];
@@ -877,7 +888,7 @@ void launch_force2(const F2Args &a, int n_items, int n, cudaStream_t s) {
   b.n_items = n_items;
   b.k1875 = 1.875;
   b.k0375 = 0.375;
-  force2_kernel<SPH_MINB_F2><<<pair_grid(n_items), kWarpsPerCta * 32, 0, s>>>(b);
+  force2_kernel<SPH_MINB_F2><<<(n_items + kF2W - 1) / kF2W, kF2W * 32, 0, s>>>(b);
 }
 
 // j-view builders: gather the sweep's j fields into ilist order (+ hoisted invariants).
@@ -936,10 +947,11 @@ void launch_density_fast(const DenArgs &a, int n_items, bool aos, cudaStream_t s
   const int G = pair_grid(n_items), B = kWarpsPerCta * 32;
   if (b.boxes && b.jlist && b.jv2.x && !aos) {
     b.k0375 = 0.375;
+    const int G2 = (n_items + kD2W - 1) / kD2W, B2 = kD2W * 32;
     switch (b.jslices) {
-    case 2: density2_kernel<SPH_MINB_D2, 2><<<G, B, 0, s>>>(b); break;
-    case 4: density2_kernel<SPH_MINB_D2, 4><<<G, B, 0, s>>>(b); break;
-    default: density2_kernel<SPH_MINB_D2, 1><<<G, B, 0, s>>>(b); break;
+    case 2: density2_kernel<SPH_MINB_D2, 2><<<G2, B2, 0, s>>>(b); break;
+    case 4: density2_kernel<SPH_MINB_D2, 4><<<G2, B2, 0, s>>>(b); break;
+    default: density2_kernel<SPH_MINB_D2, 1><<<G2, B2, 0, s>>>(b); break;
     }
   } else if (b.boxes && b.jlist) {
     if (aos) density_cull_kernel<FastPolicy, true><<<G, B, 0, s>>>(b);
