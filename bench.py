@@ -453,6 +453,13 @@ def _finish(out, ctx, store, grid, par, args, rank, world, ph, names, den_eval, 
         }
         out["roofline_density"] = {"achieved": ach_d, "frac": ach_d / fp64,
                                    "flops_per_pair": dfl, "unit": "TFLOP/s"}
+        # the north-star figure: the whole step (density rounds + force + linear kernels +
+        # rebin) against the FP64 pipe, algorithmic flops of the pair sweeps per step
+        step_flops = dfl * (den_eval / args.steps) + ffl * fpairs
+        ach_s = step_flops / (float(np.sum(ph)) * 1e-3) / 1e12
+        out["roofline_step"] = {"achieved": ach_s, "peak": fp64, "frac": ach_s / fp64,
+                                "unit": "TFLOP/s", "flops_per_step": step_flops,
+                                "ms_per_step": float(np.sum(ph))}
         hbm = peaks.get("hbm_gbs", 6650.0)
         out["roofline_linear"] = {
             k: {"achieved_gbs": LINEAR_BYTES[k] * args.n / (ph[names.index(k)] * 1e-3) / 1e9,
