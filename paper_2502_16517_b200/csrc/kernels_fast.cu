@@ -729,14 +729,23 @@ __device__ __forceinline__ void density2_pair(const FastPolicy::DI &I, const D2T
 // h-iteration rounds >= 1, ~12 % of a cell), so culling and the in-support union stay as
 // tight as in round 0. Lane slice q takes j = q, q + JS, ... of each tile; the JS partial
 // sums are combined with shuffles at the end.
+#ifndef SPH_D2_COMPACT
+#define SPH_D2_COMPACT 1
+#endif
+
 template <int MINB, int JS>
 __global__ void __launch_bounds__(kD2W * 32, MINB) density2_kernel(DenArgs A) {
-  __shared__ D2Tile tiles[kD2W][2];
+  // [0], [1]: cp.async staging double buffer; [2]: the staged chunk's j's that can reach
+  // the warp (compacted), which the pair loop consumes
+  __shared__ D2Tile tiles[kD2W][2 + SPH_D2_COMPACT];
   __shared__ ActiveLayout lay[kD2W];
   const int w = warp_in_cta(), lane = lane_id();
   const int item_idx = blockIdx.x * kD2W + w;
   if (item_idx >= A.n_items) return;
-  if (lane < 18) tiles[w][0].spl[lane] = tiles[w][1].spl[lane] = kSplPE[lane];
+  if (lane < 18) {
+#pragma unroll
+    for (int b = 0; b < 2 + SPH_D2_COMPACT; ++b) tiles[w][b].spl[lane] = kSplPE[lane];
+  }
   ActiveLayout &L = lay[w];
   const Item it = A.items[item_idx];
   if (lane == 0) build_active(A.g, it.cell, L);
@@ -782,11 +791,42 @@ __global__ void __launch_bounds__(kD2W * 32, MINB) density2_kernel(DenArgs A) {
       }
       staged = has_next;
       __syncwarp();
-      const D2Tile &T = tiles[w][buf];
+      // per-j culling: a j farther than the warp's reach from the warp box can be in no
+      // lane's support (same test as chunk_near, per particle); the others are compacted
+      // into tiles[w][2], padded with inert dummies to the pair loop's granule
+      int nj = kTJ;
+      const D2Tile *Tp = &tiles[w][buf];
+      if constexpr (SPH_D2_COMPACT && JS == 1) { // (rounds >= 1 with j-slices: measured slower)
+        constexpr int PADQ = JS * ((kTJ / JS) < 4 ? (kTJ / JS) : 4); // pair-loop granule
+        const D2Tile &S = tiles[w][buf];
+        D2Tile &C = tiles[w][2];
+        const float jx = (float)S.x[lane] + (float)L.sx[cnb], jy = (float)S.y[lane] + (float)L.sy[cnb];
+        const float gx = fmaxf(0.0f, fmaxf(jx - ixhi, ixlo - jx));
+        const float gy = fmaxf(0.0f, fmaxf(jy - iyhi, iylo - jy));
+        const bool rel = gx * gx + gy * gy <= reach2;
+        const unsigned rm = __ballot_sync(0xffffffffu, rel);
+        nj = __popc(rm);
+        const int pos = rel ? __popc(rm & ((1u << lane) - 1u)) : nj + __popc(~rm & ((1u << lane) - 1u));
+        if (rel) {
+          C.x[pos] = S.x[lane];
+          C.y[pos] = S.y[lane];
+          C.m[pos] = S.m[lane];
+          C.vv[pos] = S.vv[lane];
+        } else if (pos < ((nj + PADQ - 1) / PADQ) * PADQ) {
+          C.x[pos] = kDummyX;
+          C.y[pos] = kDummyX;
+          C.m[pos] = 0.0;
+          C.vv[pos] = make_double2(0.0, 0.0);
+        }
+        nj = ((nj + PADQ - 1) / PADQ) * PADQ;
+        __syncwarp();
+        Tp = &tiles[w][2];
+      }
+      const D2Tile &T = *Tp;
       const double xs = xi.x - L.sx[cnb], ys = xi.y - L.sy[cnb]; // periodic image, i side
       if constexpr (JS == 1) {
 #pragma unroll 1
-        for (int j = 0; j < kTJ; j += 4) {
+        for (int j = 0; j < nj; j += 4) {
           double dx[4], dy[4], r2[4];
           {
             const double2 X0 = *reinterpret_cast<const double2 *>(&T.x[j]);
@@ -805,7 +845,7 @@ __global__ void __launch_bounds__(kD2W * 32, MINB) density2_kernel(DenArgs A) {
       } else {
         constexpr int U = (kTJ / JS) < 4 ? (kTJ / JS) : 4;
 #pragma unroll 1
-        for (int t = 0; t < kTJ / JS; t += U) {
+        for (int t = 0; t * JS < nj; t += U) {
           double dx[U], dy[U], r2[U];
 #pragma unroll
           for (int u = 0; u < U; ++u) {
