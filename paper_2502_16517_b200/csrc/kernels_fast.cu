@@ -24,7 +24,7 @@ namespace sphb {
 namespace {
 
 // x^(-1/2) and x^(-3/2) to ~1 ulp from the MUFU seed y0 = rsqrt.approx.f64(x), whose
-// relative error is below 2^-20 (measured on B200, tools/rsq_probe). With e = 1 - x y0^2
+// relative error is below 2^-20 (measured on B200, tools/fp64_micro.cu). With e = 1 - x y0^2
 // (|e| < 2^-19; y0 has 21 significant bits so y0^2 is exact and e is rounded once):
 //   x^(-1/2) = y0 (1 + e/2 + 3e^2/8 + O(e^3)),   x^(-3/2) = y0^3 (1 + 3e/2 + 15e^2/8 + O(e^3)),
 // truncation < 2^-55. 5 (resp. 6) FP64 ops instead of Newton's 7 (resp. 9).
@@ -444,6 +444,9 @@ constexpr int kF2W = SPH_F2_WPC, kD2W = SPH_D2_WPC;
 
 // SPH part of force_pair (kernels.cpp:132-152) for one in-support pair: accumulates u_dt,
 // h_dt, v_sig and returns the SPH radial factor A*g (the caller applies K).
+#ifndef SPH_F2_XI_RELOAD
+#define SPH_F2_XI_RELOAD 0 // 1: re-read x_i per chunk (L1 hit) instead of keeping it live (measured: noise)
+#endif
 #ifndef SPH_F2_QFREE
 #define SPH_F2_QFREE 1 // spline row from r2 vs per-i thresholds, s = fma(+-1/h, r, c_off)
 #endif
@@ -462,10 +465,11 @@ __device__ __forceinline__ double force2_sph(const F2I &I, const F2Tile &T, int 
   const int hr = __double2hiint(r2);
   int row = hr < I.hiQ15 ? 3 : 0;
   if (hr < I.hiQ05) row = 6;
-  const double2 t0 = T.spl[row], t1 = T.spl[row + 1], t2 = T.spl[row + 2];
+  const double c_off = T.spl[row].x;
+  const double2 t1 = T.spl[row + 1], t2 = T.spl[row + 2];
   const double sih = __hiloint2double(__double2hiint(I.inv_hi) ^ (row == 6 ? 0 : (int)0x80000000),
                                       __double2loint(I.inv_hi));
-  const double s = fma(sih, r2 * rinv, t0.x);
+  const double s = fma(sih, r2 * rinv, c_off);
 #else
   const double q = r2 * rinv * I.inv_hi;
   const int hq = __double2hiint(q);
@@ -581,7 +585,12 @@ __global__ void __launch_bounds__(kF2W * 32, MINB) force2_kernel(F2Args A) {
       staged = has_next;
       __syncwarp();
       const F2Tile &T = tiles[w][buf];
-      const double xs = xi.x - L.sx[cnb], ys = xi.y - L.sy[cnb]; // periodic image, i side
+      #if SPH_F2_XI_RELOAD
+      const double2 xr = A.soa.x[slot];
+#else
+      const double2 xr = xi;
+#endif
+      const double xs = xr.x - L.sx[cnb], ys = xr.y - L.sy[cnb]; // periodic image, i side
       if ((nmask >> b) & 1u) {
 #pragma unroll 1
         for (int j = 0; j < kTJ; j += 2) {

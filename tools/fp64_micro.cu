@@ -3,6 +3,7 @@
 // warps per SM and independent chains per warp, whether MUFU.RSQ64H slows a DFMA stream, and
 // the pair rate a gravity-style chain reaches against warps per SM and pairs per step.
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o tools/fp64_micro tools/fp64_micro.cu
+#include <cmath>
 #include <cstdio>
 #include <cuda_runtime.h>
 
@@ -68,6 +69,29 @@ __global__ void mufu_mix(double *out, double a, double b, int iters) {
     }
   }
   out[blockIdx.x * blockDim.x + threadIdx.x] = x[0] + x[1] + x[2] + x[3] + acc;
+}
+
+// accuracy of the MUFU seed and of the series-corrected x^-1/2, x^-3/2 used by the FAST
+// pair kernels (kernels_fast.cu): max relative error over x = 2^u, u uniform in [-40, 10)
+__global__ void rsq_accuracy(double *out, int n) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  double e_seed = 0, e_half = 0, e_three = 0;
+  for (int k = t; k < n; k += gridDim.x * blockDim.x) {
+    const double u = -40.0 + 50.0 * ((k * 0.6180339887498949) - floor(k * 0.6180339887498949));
+    const double x = exp2(u);
+    const double ref = 1.0 / sqrt(x), ref3 = ref * ref * ref;
+    const double y0 = rsq64h(x);
+    const double e = fma(-x, y0 * y0, 1.0);
+    const double y = fma(y0, e * fma(e, 0.375, 0.5), y0);
+    const double tt = y0 * y0, y3 = tt * y0;
+    const double z = fma(y3, e * fma(e, 1.875, 1.5), y3);
+    e_seed = fmax(e_seed, fabs(y0 - ref) / ref);
+    e_half = fmax(e_half, fabs(y - ref) / ref);
+    e_three = fmax(e_three, fabs(z - ref3) / ref3);
+  }
+  out[3 * t] = e_seed;
+  out[3 * t + 1] = e_half;
+  out[3 * t + 2] = e_three;
 }
 
 // far-gravity body (13 FP64 + MUFU per pair), G independent pairs per step, pairs per thread
@@ -183,6 +207,19 @@ int main() {
       printf("gravity warps/SM %2d G %d: %.3e pairs/s = %.2f FP64 instr-equiv TFLOP/s (13/pair)\n", wps, G,
              pairs / ms * 1e3, pairs * 13 * 2 / ms / 1e9);
     }
+  }
+  {
+    const int blocks = 148, threads = 256, n = 1 << 24;
+    rsq_accuracy<<<blocks, threads>>>(out, n);
+    CK(cudaDeviceSynchronize());
+    static double h[3 * 148 * 256];
+    cudaMemcpy(h, out, sizeof h, cudaMemcpyDeviceToHost);
+    double m[3] = {0, 0, 0};
+    for (int k = 0; k < blocks * threads; ++k)
+      for (int q = 0; q < 3; ++q) m[q] = m[q] > h[3 * k + q] ? m[q] : h[3 * k + q];
+    printf("rsqrt.approx.f64 seed max rel err %.3e (2^%.2f); x^-1/2 series %.3e (%.2f ulp); "
+           "x^-3/2 series %.3e (%.2f ulp, vs a 1/sqrt reference that itself carries ~1.5 ulp)\n",
+           m[0], log2(m[0]), m[1], m[1] / 1.1102230246251565e-16, m[2], m[2] / 1.1102230246251565e-16);
   }
   CK(cudaDeviceSynchronize());
   return 0;
