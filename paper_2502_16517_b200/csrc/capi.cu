@@ -228,6 +228,18 @@ struct sph_ctx {
   bool need_rebin = false; // particles were appended: cell lists stale until sph_rebin
   DevBuf<unsigned char> dd_mask, dd_flag;
   DevBuf<int> dd_sel, dd_cnt;
+  DevBuf<int> mi_k, mi_off;
+  DevBuf<char> mi_tmp;
+  ItemsScratch mi{};
+  const ItemsScratch *items_scratch() {
+    mi_k.ensure(ncells);
+    mi_off.ensure(ncells);
+    const size_t tb = make_items_scratch_bytes(ncells);
+    mi_tmp.ensure(tb);
+    mi = ItemsScratch{mi_k.p, mi_off.p, mi_tmp.p, tb};
+    launched(3); // counts + scan + write instead of one single-block kernel
+    return &mi;
+  }
   int64_t active_pairs = 0;
 
   // mirror state
@@ -268,6 +280,8 @@ struct sph_ctx {
     items_b.release(); hcur.release(); wc.release(); rounds.release(); dense.release();
     cub_tmp.release(); h_stage.release(); h_small.release(); owned.release();
     items_g.release(); hdep.release();
+    dd_mask.release(); dd_flag.release(); dd_sel.release(); dd_cnt.release();
+    mi_k.release(); mi_off.release(); mi_tmp.release();
     jv_xy.release(); jv_vv.release(); jv_mg.release(); jv_pv.release(); jv_m.release(); jv_c.release();
     jv2_x.release(); jv2_y.release(); jv2_gm.release(); jv2_vv.release(); jv2_pv.release();
     jv2_cm.release(); jv2_m.release();
@@ -353,7 +367,7 @@ struct sph_ctx {
     const bool aos_src = !soa_ahead;
     launch_spatial_order(ilist.p, aos.p, soa, aos_src, cell_begin.p, ncells, nx, ny, stream);
     launch_make_items(items0.p, scalars.p, pairs_dev.p, cnt.p, cell_begin.p, na_cell.p,
-                      cell_order.p, ncells, stream);
+                      cell_order.p, ncells, stream, kTI, items_scratch());
     launched(3);
     CK(cudaMemcpyAsync(h_small.p, scalars.p, sizeof(int), cudaMemcpyDeviceToHost, stream));
     CK(cudaMemcpyAsync((char *)h_small.p + 8, pairs_dev.p, sizeof(long long),
@@ -428,7 +442,7 @@ struct sph_ctx {
     items_b.ensure((size_t)ncells + (size_t)n / (kTI / std::max(js0, js1)) + 1);
     if (js0 > 1) { // round-0 items of 32/js0 particles
       launch_make_items(items_b.p, scalars.p, pairs_dev.p, cnt.p, cell_begin.p, na_cell.p,
-                        cell_order.p, ncells, stream, kTI / js0);
+                        cell_order.p, ncells, stream, kTI / js0, items_scratch());
       launched();
       CK(cudaMemcpyAsync(h_small.p, scalars.p, sizeof(int), cudaMemcpyDeviceToHost, stream));
       CK(cudaStreamSynchronize(stream));
@@ -458,7 +472,7 @@ struct sph_ctx {
       launch_compact_pending(pend_out, cnt_out, list, cnt_cur, again.p, cell_begin.p, ncells,
                              stream);
       launch_make_items(items_next, scalars.p, pairs_dev.p, cnt_out, cell_begin.p, na_cell.p,
-                        cell_order.p, ncells, stream, kTI / js1);
+                        cell_order.p, ncells, stream, kTI / js1, items_scratch());
       launched(3);
       pairs_total += pairs;
       max_round = r + 1;
@@ -564,7 +578,7 @@ struct sph_ctx {
     // grid-order items and the per-cell item prefix (host)
     items_g.ensure((size_t)ncells + (size_t)n / kTI + 1);
     launch_make_items(items_g.p, scalars.p, pairs_dev.p, cnt.p, cell_begin.p, na_cell.p, nullptr,
-                      ncells, stream);
+                      ncells, stream, kTI, items_scratch());
     launched();
     std::vector<int> cb(ncells + 1);
     CK(cudaMemcpyAsync(cb.data(), cell_begin.p, sizeof(int) * (ncells + 1), cudaMemcpyDeviceToHost,
@@ -966,7 +980,10 @@ struct sph_ctx {
   // when they hold data.
   void apply_perm(const int *perm, int64_t m) {
     aos_tmp.ensure(m);
-    launch_permute<Particle>(aos_tmp.p, aos.p, perm, (int)m, stream);
+    if (soa_ahead) // the SoA is the truth: move only the AoS-only fields
+      launch_permute_record_tails(aos_tmp.p, aos.p, perm, (int)m, stream);
+    else
+      launch_permute<Particle>(aos_tmp.p, aos.p, perm, (int)m, stream);
     std::swap(aos.p, aos_tmp.p);
     std::swap(aos.cap, aos_tmp.cap);
     host_idx_tmp.ensure(m);

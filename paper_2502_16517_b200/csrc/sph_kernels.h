@@ -72,9 +72,15 @@ void launch_spatial_order(int *ilist, const Particle *aos, const SoaMirror &f, b
 // work items from per-cell counts: items for cell c cover list[cell_begin[c] + k*kTI ...];
 // out2[0] = n_items, out2[1] = pair count (sum cnt_c * na_c, int64 split in two ints)
 // Items are emitted in `order` (cells sorted by descending cost bucket; may be null).
+struct ItemsScratch {
+  int *k, *off;     // ncells each
+  void *tmp;        // cub scan temporary storage
+  size_t tmp_bytes; // >= make_items_scratch_bytes(ncells)
+};
+size_t make_items_scratch_bytes(int ncells);
 void launch_make_items(Item *items, int *n_items_out, long long *pairs_out, const int *cnt,
                        const int *cell_begin, const int *na_cell, const int *order, int ncells,
-                       cudaStream_t s, int tile = 32);
+                       cudaStream_t s, int tile = 32, const ItemsScratch *scr = nullptr);
 // FP32 bounding boxes of the 32-chunks of each cell's ilist (culled FAST density)
 void launch_chunk_boxes(float4 *boxes, const int *ilist, const Particle *aos, const SoaMirror &f,
                         bool aos_src, const int *cell_begin, int ncells, cudaStream_t s);
@@ -97,6 +103,9 @@ void launch_cell_begin_from_sorted(int *cell_begin, const unsigned long long *ke
                                    int ncells, cudaStream_t s);
 template <class T>
 void launch_permute(T *dst, const T *src, const int *perm, int n, cudaStream_t s);
+// record pieces of the fields without a SoA array only (id, cell, dbg[1], spare)
+void launch_permute_record_tails(Particle *dst, const Particle *src, const int *perm, int n,
+                                 cudaStream_t s);
 void launch_set_cell(Particle *aos, const int *cell_begin, int ncells, cudaStream_t s);
 // FP64 DFMA throughput probe
 void launch_fp64_probe(double *out, int blocks, int iters, cudaStream_t s);
