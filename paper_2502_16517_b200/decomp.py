@@ -286,25 +286,29 @@ class DeviceSlabSim:
             import torch.distributed as dist
             self.dist = dist
             self.nccl = dist.get_backend(group) == "nccl"
-        nx = decomp.nx
-        self.mine = np.zeros(nx, np.uint8)
-        self.mine[decomp.owned_cols()] = 1
-        self.not_mine = (1 - self.mine).astype(np.uint8)
-        self.peers = decomp.neighbours()
-        self.cols_of = {}   # columns owned by peer q (migration destinations)
-        self.send_to = {}   # my columns in q's halo
-        self.halo_from = {}  # my halo columns owned by q
-        for q in self.peers:
-            m = np.zeros(nx, np.uint8)
-            m[decomp.owned_cols(q)] = 1
-            self.cols_of[q] = m
-            s = np.zeros(nx, np.uint8)
-            s[decomp.send_cols(q)] = 1
-            self.send_to[q] = s
-            h = np.zeros(nx, np.uint8)
-            h[np.intersect1d(decomp.halo_cols(), decomp.owned_cols(q))] = 1
-            self.halo_from[q] = h
+        m = self.masks(decomp)
+        self.mine, self.not_mine, self.peers = m["mine"], m["not_mine"], m["peers"]
+        self.cols_of, self.send_to, self.halo_from = m["cols_of"], m["send_to"], m["halo_from"]
         self.bytes_sent = 0
+
+    @staticmethod
+    def masks(decomp: SlabDecomposition) -> dict:
+        """Column masks (nx bytes) of one rank: its own columns, the rest, and per neighbour
+        q the columns q owns (migration), my columns in q's halo (halo / rho send) and my
+        halo columns owned by q (halo / rho receive)."""
+        nx = decomp.nx
+        mine = np.zeros(nx, np.uint8)
+        mine[decomp.owned_cols()] = 1
+        out = {"mine": mine, "not_mine": (1 - mine).astype(np.uint8),
+               "peers": decomp.neighbours(), "cols_of": {}, "send_to": {}, "halo_from": {}}
+        for q in out["peers"]:
+            for key, cols in (("cols_of", decomp.owned_cols(q)),
+                              ("send_to", decomp.send_cols(q)),
+                              ("halo_from", np.intersect1d(decomp.halo_cols(), decomp.owned_cols(q)))):
+                mk = np.zeros(nx, np.uint8)
+                mk[cols] = 1
+                out[key][q] = mk
+        return out
 
     @staticmethod
     def start(ctx, decomp: SlabDecomposition) -> None:

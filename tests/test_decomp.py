@@ -211,3 +211,23 @@ def test_device_resident_decomposition_fast_equals_one_rank(world):
     one = _run_dev(1, "Fast")
     many = _run_dev(world, "Fast")
     assert many.tobytes() == one.tobytes()
+
+
+@pytest.mark.parametrize("nx,world", [(9, 2), (17, 3), (45, 4), (128, 8), (90, 4)])
+def test_device_slab_masks_are_consistent(nx, world):
+    """The column masks DeviceSlabSim moves buffers with: what rank r sends to q is exactly
+    what q expects from r (halo and rho refresh), the migration targets cover every column
+    outside the slab that a one-column move can reach, and the slabs partition the grid."""
+    from paper_2502_16517_b200.decomp import DeviceSlabSim
+    ms = [DeviceSlabSim.masks(SlabDecomposition(nx, nx, world, r)) for r in range(world)]
+    assert np.array_equal(sum(m["mine"].astype(int) for m in ms), np.ones(nx, int))
+    for r, m in enumerate(ms):
+        for q in m["peers"]:
+            assert r in ms[q]["peers"]
+            assert np.array_equal(m["send_to"][q], ms[q]["halo_from"][r])
+            assert not np.any(m["send_to"][q] & ~m["mine"].astype(bool))
+            assert np.array_equal(m["cols_of"][q], ms[q]["mine"])
+        # the columns adjacent to the slab (where a migrating particle can land) belong to peers
+        cols = np.nonzero(m["mine"])[0]
+        for c in ((cols[0] - 1) % nx, (cols[-1] + 1) % nx):
+            assert any(m["cols_of"][q][c] for q in m["peers"])
