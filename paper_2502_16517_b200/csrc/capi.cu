@@ -418,10 +418,10 @@ struct sph_ctx {
       launched();
       A.boxes = boxes.p;
       A.jlist = ilist.p;
-      if (force2 && !use_aos && A.g.use_shift) { // issue-lean density over the SoA mirror
+      if (force2 && A.g.use_shift) { // issue-lean density (any layout)
         jv2_x.ensure(n); jv2_y.ensure(n); jv2_m.ensure(n); jv2_vv.ensure(n);
         A.jv2 = D2View{jv2_x.p, jv2_y.p, jv2_m.p, jv2_vv.p};
-        launch_jview_density2(A.jv2, ilist.p, soa, (int)n, stream);
+        launch_jview_density2(A.jv2, ilist.p, aos.p, soa, use_aos, (int)n, stream);
       } else {
         jv_xy.ensure(n); jv_vv.ensure(n); jv_m.ensure(n);
         launch_jview_density(jv_xy.p, jv_vv.p, jv_m.p, ilist.p, aos.p, soa, use_aos, (int)n, stream);
@@ -510,10 +510,10 @@ struct sph_ctx {
     A.grav = par.grav;
     A.aos = aos.p;
     A.soa = soa;
-    if (!exact && cull && force2 && !use_aos && A.g.use_shift) {
-      // issue-lean kernel over the SoA mirror (spatial j order, far chunks gravity-only)
+    if (!exact && cull && force2 && A.g.use_shift) {
+      // issue-lean kernel (spatial j order, far chunks gravity-only), any layout
       boxes.ensure((size_t)n / 32 + (size_t)ncells + 2);
-      launch_chunk_boxes(boxes.p, ilist.p, aos.p, soa, false, cell_begin.p, ncells, stream);
+      launch_chunk_boxes(boxes.p, ilist.p, aos.p, soa, use_aos, cell_begin.p, ncells, stream);
       jv2_x.ensure(n); jv2_y.ensure(n); jv2_gm.ensure(n);
       jv2_vv.ensure(n); jv2_pv.ensure(n); jv2_cm.ensure(n);
       F2Args B{};
@@ -521,6 +521,7 @@ struct sph_ctx {
       B.items = items0.p;
       B.list = ilist.p;
       B.grav = par.grav;
+      B.aos = use_aos ? aos.p : nullptr;
       B.soa = soa;
       B.boxes = boxes.p;
       B.jv = F2View{jv2_x.p, jv2_y.p, jv2_gm.p, jv2_vv.p, jv2_pv.p, jv2_cm.p};

@@ -516,7 +516,7 @@ __device__ __forceinline__ void force2_stage(F2Tile &T, const ActiveLayout &L, c
   cp_async_commit();
 }
 
-template <int MINB>
+template <int MINB, bool AOS>
 __global__ void __launch_bounds__(kF2W * 32, MINB) force2_kernel(F2Args A) {
   __shared__ F2Tile tiles[kF2W][2];
   __shared__ ActiveLayout lay[kF2W];
@@ -529,16 +529,17 @@ __global__ void __launch_bounds__(kF2W * 32, MINB) force2_kernel(F2Args A) {
   if (lane == 0) build_active(A.g, it.cell, L);
   const bool live = lane < it.count;
   const int slot = A.list[it.start + (live ? lane : 0)];
-  const double2 xi = A.soa.x[slot];
-  const double hi = A.soa.h[slot];
+  JSrc<AOS> src; // i side: the AoS records in place or the SoA mirror
+  if constexpr (AOS) src.p = A.aos; else src.f = A.soa;
+  const double2 xi = src.x(slot);
+  const double hi = src.h(slot);
   F2I I;
   double eps2, K;
   unsigned hiH2m1;
   {
     const FastPolicy::FI F =
-        FastPolicy::for_i(xi, A.soa.vp[slot], hi, A.soa.p[slot], A.soa.rho[slot],
-                          A.soa.rho_dh[slot], A.soa.c[slot], A.soa.div_v[slot],
-                          A.soa.rot_v[slot], A.grav, nullptr);
+        FastPolicy::for_i(xi, src.vp(slot), hi, src.pr(slot), src.rho(slot), src.rho_dh(slot),
+                          src.c(slot), src.div_v(slot), src.rot_v(slot), A.grav, nullptr);
     I = F2I{F.vx, F.vy, F.inv_hi, F.pri, F.mb3, __double2hiint(0.25 * hi * hi),
             __double2hiint(2.25 * hi * hi)};
     eps2 = F.eps2;
@@ -586,7 +587,7 @@ __global__ void __launch_bounds__(kF2W * 32, MINB) force2_kernel(F2Args A) {
       __syncwarp();
       const F2Tile &T = tiles[w][buf];
       #if SPH_F2_XI_RELOAD
-      const double2 xr = A.soa.x[slot];
+      const double2 xr = src.x(slot);
 #else
       const double2 xr = xi;
 #endif
@@ -653,15 +654,20 @@ __global__ void __launch_bounds__(kF2W * 32, MINB) force2_kernel(F2Args A) {
   if (!live) return;
   // publish (force_inv terms recomputed from memory: keeps c_i, h_i out of the loop)
   const FastPolicy::FI F =
-      FastPolicy::for_i(xi, A.soa.vp[slot], hi, A.soa.p[slot], A.soa.rho[slot], A.soa.rho_dh[slot],
-                        A.soa.c[slot], A.soa.div_v[slot], A.soa.rot_v[slot], A.grav, nullptr);
-  FastPolicy::FA s{ax, ay, udt, vsig, hdt, A.soa.h_dt[slot]};
+      FastPolicy::for_i(xi, src.vp(slot), hi, src.pr(slot), src.rho(slot), src.rho_dh(slot),
+                        src.c(slot), src.div_v(slot), src.rot_v(slot), A.grav, nullptr);
+  FastPolicy::FA s{ax, ay, udt, vsig, hdt, src.h_dt(slot)};
   double o[5];
   FastPolicy::for_publish(F, s, o);
-  A.soa.a[slot] = make_double2(o[0], o[1]);
-  A.soa.u_dt[slot] = o[2];
-  A.soa.v_sig[slot] = o[3];
-  A.soa.h_dt[slot] = o[4];
+  if constexpr (AOS) {
+    Particle &q = const_cast<Particle &>(A.aos[slot]);
+    q.a[0] = o[0]; q.a[1] = o[1]; q.u_dt = o[2]; q.v_sig = o[3]; q.h_dt = o[4];
+  } else {
+    A.soa.a[slot] = make_double2(o[0], o[1]);
+    A.soa.u_dt[slot] = o[2];
+    A.soa.v_sig[slot] = o[3];
+    A.soa.h_dt[slot] = o[4];
+  }
 }
 
 // ---------------------------------------------------------------------------------------
@@ -742,7 +748,7 @@ __device__ __forceinline__ void density2_pair(const FastPolicy::DI &I, const D2T
 #define SPH_D2_COMPACT 1
 #endif
 
-template <int MINB, int JS>
+template <int MINB, int JS, bool AOS>
 __global__ void __launch_bounds__(kD2W * 32, MINB) density2_kernel(DenArgs A) {
   // [0], [1]: cp.async staging double buffer; [2]: the staged chunk's j's that can reach
   // the warp (compacted), which the pair loop consumes
@@ -761,8 +767,10 @@ __global__ void __launch_bounds__(kD2W * 32, MINB) density2_kernel(DenArgs A) {
   const int iw = lane / JS, qs = lane % JS;
   const bool live = iw < it.count;
   const int slot = A.list[it.start + (live ? iw : 0)];
-  const double2 xi = A.soa.x[slot], vi = A.soa.vp[slot];
-  const double h = (A.round == 0) ? A.soa.h[slot] : A.hcur[slot];
+  JSrc<AOS> src; // i side: the AoS records in place or the SoA mirror
+  if constexpr (AOS) src.p = A.aos; else src.f = A.soa;
+  const double2 xi = src.x(slot), vi = src.vp(slot);
+  const double h = (A.round == 0) ? src.h(slot) : A.hcur[slot];
   const FastPolicy::DI I = FastPolicy::den_i(xi.x, xi.y, vi.x, vi.y, h);
   FastPolicy::DA s = FastPolicy::den_zero();
   const float ixlo = warp_min((float)xi.x), ixhi = warp_max((float)xi.x);
@@ -892,52 +900,74 @@ __global__ void __launch_bounds__(kD2W * 32, MINB) density2_kernel(DenArgs A) {
     return;
   }
   double o[6];
-  FastPolicy::den_publish(s, h, A.soa.m[slot], o);
+  FastPolicy::den_publish(s, h, src.m(slot), o);
   if (A.rounds_out) A.rounds_out[slot] = (unsigned char)(A.round + 1);
-  A.soa.h[slot] = o[0]; A.soa.rho[slot] = o[1]; A.soa.wcount[slot] = o[2];
-  A.soa.rho_dh[slot] = o[3]; A.soa.rot_v[slot] = o[4]; A.soa.div_v[slot] = o[5];
-  if (st == 2) A.soa.flags[slot] += 1;
+  if constexpr (AOS) {
+    Particle &q = const_cast<Particle &>(A.aos[slot]);
+    q.h = o[0]; q.rho = o[1]; q.wcount = o[2]; q.rho_dh = o[3]; q.rot_v = o[4]; q.div_v = o[5];
+    if (st == 2) q.flags += 1;
+  } else {
+    A.soa.h[slot] = o[0]; A.soa.rho[slot] = o[1]; A.soa.wcount[slot] = o[2];
+    A.soa.rho_dh[slot] = o[3]; A.soa.rot_v[slot] = o[4]; A.soa.div_v[slot] = o[5];
+    if (st == 2) A.soa.flags[slot] += 1;
+  }
 }
 
-__global__ void jview_density2_kernel(D2View v, const int *ilist, SoaMirror f, int n) {
+template <bool AOS>
+__global__ void jview_density2_kernel(D2View v, const int *ilist, const Particle *aos, SoaMirror f,
+                                      int n) {
   const int p = blockIdx.x * blockDim.x + threadIdx.x;
   if (p >= n) return;
+  JSrc<AOS> src;
+  if constexpr (AOS) src.p = aos; else src.f = f;
   const int sj = ilist[p];
-  const double2 x = f.x[sj];
+  const double2 x = src.x(sj);
   const_cast<double *>(v.x)[p] = x.x;
   const_cast<double *>(v.y)[p] = x.y;
-  const_cast<double *>(v.m)[p] = f.m[sj];
-  const_cast<double2 *>(v.vv)[p] = f.vp[sj];
+  const_cast<double *>(v.m)[p] = src.m(sj);
+  const_cast<double2 *>(v.vv)[p] = src.vp(sj);
 }
 
-void launch_jview_density2(const D2View &v, const int *ilist, const SoaMirror &f, int n,
-                           cudaStream_t s) {
-  if (n > 0) jview_density2_kernel<<<(n + 255) / 256, 256, 0, s>>>(v, ilist, f, n);
+void launch_jview_density2(const D2View &v, const int *ilist, const Particle *aos,
+                           const SoaMirror &f, bool use_aos, int n, cudaStream_t s) {
+  if (n <= 0) return;
+  if (use_aos) jview_density2_kernel<true><<<(n + 255) / 256, 256, 0, s>>>(v, ilist, aos, f, n);
+  else jview_density2_kernel<false><<<(n + 255) / 256, 256, 0, s>>>(v, ilist, aos, f, n);
 }
 
-__global__ void jview_force2_kernel(F2View v, const int *ilist, SoaMirror f, int n, double grav) {
+template <bool AOS>
+__global__ void jview_force2_kernel(F2View v, const int *ilist, const Particle *aos, SoaMirror f,
+                                    int n, double grav) {
   const int p = blockIdx.x * blockDim.x + threadIdx.x;
   if (p >= n) return;
+  JSrc<AOS> src;
+  if constexpr (AOS) src.p = aos; else src.f = f;
   const int sj = ilist[p];
-  const double2 x = f.x[sj];
-  const double m = f.m[sj], rho = f.rho[sj];
-  const double4 d = FastPolicy::stage_force(m, rho, f.p[sj], grav); // (m, gm, P, V)
+  const double2 x = src.x(sj);
+  const double m = src.m(sj), rho = src.rho(sj);
+  const double4 d = FastPolicy::stage_force(m, rho, src.pr(sj), grav); // (m, gm, P, V)
   const_cast<double *>(v.x)[p] = x.x;
   const_cast<double *>(v.y)[p] = x.y;
   const_cast<double *>(v.gm)[p] = d.y;
-  const_cast<double2 *>(v.vv)[p] = f.vp[sj];
+  const_cast<double2 *>(v.vv)[p] = src.vp(sj);
   const_cast<double2 *>(v.pv)[p] = make_double2(d.z, d.w);
-  const_cast<double2 *>(v.cm)[p] = make_double2(f.c[sj], m);
+  const_cast<double2 *>(v.cm)[p] = make_double2(src.c(sj), m);
 }
 
 void launch_force2(const F2Args &a, int n_items, int n, cudaStream_t s) {
-  if (n > 0) jview_force2_kernel<<<(n + 255) / 256, 256, 0, s>>>(a.jv, a.list, a.soa, n, a.grav);
+  const bool aos = a.aos != nullptr;
+  if (n > 0) {
+    if (aos) jview_force2_kernel<true><<<(n + 255) / 256, 256, 0, s>>>(a.jv, a.list, a.aos, a.soa, n, a.grav);
+    else jview_force2_kernel<false><<<(n + 255) / 256, 256, 0, s>>>(a.jv, a.list, a.aos, a.soa, n, a.grav);
+  }
   if (n_items <= 0) return;
   F2Args b = a;
   b.n_items = n_items;
   b.k1875 = 1.875;
   b.k0375 = 0.375;
-  force2_kernel<SPH_MINB_F2><<<(n_items + kF2W - 1) / kF2W, kF2W * 32, 0, s>>>(b);
+  const int G = (n_items + kF2W - 1) / kF2W;
+  if (aos) force2_kernel<SPH_MINB_F2, true><<<G, kF2W * 32, 0, s>>>(b);
+  else force2_kernel<SPH_MINB_F2, false><<<G, kF2W * 32, 0, s>>>(b);
 }
 
 // j-view builders: gather the sweep's j fields into ilist order (+ hoisted invariants).
@@ -994,13 +1024,21 @@ void launch_density_fast(const DenArgs &a, int n_items, bool aos, cudaStream_t s
   DenArgs b = a;
   b.n_items = n_items;
   const int G = pair_grid(n_items), B = kWarpsPerCta * 32;
-  if (b.boxes && b.jlist && b.jv2.x && !aos) {
+  if (b.boxes && b.jlist && b.jv2.x) {
     b.k0375 = 0.375;
     const int G2 = (n_items + kD2W - 1) / kD2W, B2 = kD2W * 32;
-    switch (b.jslices) {
-    case 2: density2_kernel<SPH_MINB_D2, 2><<<G2, B2, 0, s>>>(b); break;
-    case 4: density2_kernel<SPH_MINB_D2, 4><<<G2, B2, 0, s>>>(b); break;
-    default: density2_kernel<SPH_MINB_D2, 1><<<G2, B2, 0, s>>>(b); break;
+    if (aos) {
+      switch (b.jslices) {
+      case 2: density2_kernel<SPH_MINB_D2, 2, true><<<G2, B2, 0, s>>>(b); break;
+      case 4: density2_kernel<SPH_MINB_D2, 4, true><<<G2, B2, 0, s>>>(b); break;
+      default: density2_kernel<SPH_MINB_D2, 1, true><<<G2, B2, 0, s>>>(b); break;
+      }
+    } else {
+      switch (b.jslices) {
+      case 2: density2_kernel<SPH_MINB_D2, 2, false><<<G2, B2, 0, s>>>(b); break;
+      case 4: density2_kernel<SPH_MINB_D2, 4, false><<<G2, B2, 0, s>>>(b); break;
+      default: density2_kernel<SPH_MINB_D2, 1, false><<<G2, B2, 0, s>>>(b); break;
+      }
     }
   } else if (b.boxes && b.jlist) {
     if (aos) density_cull_kernel<FastPolicy, true><<<G, B, 0, s>>>(b);

@@ -118,6 +118,7 @@ struct F2Args {
   int n_items;
   const int *list;
   double grav;
+  const Particle *aos;  // non-null: i side read and written in the AoS records (AOS layout)
   SoaMirror soa;
   const float4 *boxes;
   F2View jv;

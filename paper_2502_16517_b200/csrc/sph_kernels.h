@@ -13,14 +13,15 @@ void launch_density_exact(const DenArgs &a, int n_items, bool aos, bool meanw, c
 void launch_force_exact(const ForArgs &a, int n_items, bool aos, cudaStream_t s);
 void launch_density_fast(const DenArgs &a, int n_items, bool aos, cudaStream_t s);
 void launch_force_fast(const ForArgs &a, int n_items, bool aos, cudaStream_t s);
-// issue-lean FAST force over the resident SoA mirror (builds its j-view first); needs the
-// per-stencil-cell periodic shift (nx, ny >= 5) and chunk boxes
+// issue-lean FAST force (builds its j-view first when n > 0); i side in the AoS records when
+// F2Args::aos is set, else the SoA mirror; needs the per-stencil-cell periodic shift
+// (nx, ny >= 5) and chunk boxes
 void launch_force2(const F2Args &a, int n_items, int n, cudaStream_t s);
 // split j-view for the issue-lean density round (density2_kernel, used by
 // launch_density_fast when DenArgs::jv2.x is set and the mirror is the SoA)
 struct D2View;
-void launch_jview_density2(const D2View &v, const int *ilist, const SoaMirror &f, int n,
-                           cudaStream_t s);
+void launch_jview_density2(const D2View &v, const int *ilist, const Particle *aos,
+                           const SoaMirror &f, bool use_aos, int n, cudaStream_t s);
 
 // FAST j-views (kernels_fast.cu): sweep j fields in ilist order with hoisted invariants
 void launch_jview_density(double2 *xy, double2 *vv, double *m, const int *ilist,

@@ -5,10 +5,11 @@ set -x
 TAG=${1:-r1}
 B="python bench.py --steps 2 --warmup 1 --e2e-steps 1 --cpu-baseline 0"
 ncu --metrics gpu__time_duration.sum --clock-control none -c 600 --csv --log-file gpurun_out/launches_$TAG.csv $B > gpurun_out/launches_$TAG.log 2>&1
-ncu --set full --clock-control none --import-source on --kernel-name-base mangled \
-    -k regex:force_kernelINS_10FastPolicy -c 1 -o gpurun_out/force_$TAG $B > /dev/null 2>&1
-ncu --set full --clock-control none --import-source on --kernel-name-base mangled \
-    -k regex:density_cull_kernelINS_10FastPolicy -c 1 -o gpurun_out/density_$TAG $B > /dev/null 2>&1
-ncu --set full --clock-control none --import-source on --kernel-name-base mangled \
-    -k regex:"kick2_kernel|drift_kernel|kick1_kernel" -s 3 -c 3 -o gpurun_out/linear_$TAG $B > /dev/null 2>&1
+# one launch of each pair sweep after the IC and the warm-up step (steady state)
+ncu --set full --clock-control none --import-source on -k regex:^force2_kernel -s 2 -c 1 \
+    -o gpurun_out/force_$TAG $B > /dev/null 2>&1
+ncu --set full --clock-control none --import-source on -k regex:^density2_kernel -s 4 -c 2 \
+    -o gpurun_out/density_$TAG $B > /dev/null 2>&1
+ncu --set full --clock-control none --import-source on \
+    -k regex:"^kick2_kernel|^drift_kernel|^kick1_kernel" -s 3 -c 3 -o gpurun_out/linear_$TAG $B > /dev/null 2>&1
 ls -la gpurun_out
