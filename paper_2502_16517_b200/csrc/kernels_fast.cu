@@ -678,14 +678,17 @@ __global__ void __launch_bounds__(kF2W * 32, MINB) force2_kernel(F2Args A) {
 struct __align__(16) D2Tile {
   double x[kTJ], y[kTJ], m[kTJ];
   double2 vv[kTJ];
-  double2 spl[18]; // rows (outer, mid, inner) x {c_off, sgn}, {e3, e2}, {e1, e0}, {c4, c3}, {c2, c1}, {c0, 0}
+  double2 spl[12]; // rows (outer, mid, inner) x {c_off, sgn}, {c4, c3}, {c2, c1}, {c0, 0}
 };
 
-// W(q) = N P(s), dW/dq = -4 N E(s) with s = c_off + sgn q (spline.hpp:12-41)
-__constant__ double2 kSplPE[18] = {
-    {2.5, -1.0}, {1.0, 0.0}, {0.0, 0.0}, {1.0, 0.0}, {0.0, 0.0}, {0.0, 0.0},         // s^4
-    {1.5, -1.0}, {-4.0, 3.0}, {3.0, 1.0}, {-4.0, 4.0}, {6.0, 4.0}, {1.0, 0.0},       // mid
-    {0.0, 1.0}, {-6.0, 0.0}, {7.5, 0.0}, {6.0, 0.0}, {-15.0, 0.0}, {14.375, 0.0},    // inner
+// W(q) = N P(s) with s = c_off + sgn q (spline.hpp:12-41); the inner piece uses s = -q (P is
+// even there), so on every piece dW/dq = -N dP/ds and the kernel derivative is
+// E = P'(s) / 4, evaluated by the derivative Horner recursion alongside P: four table loads
+// instead of six, the same seven DFMA. Sums over m E carry the factor 4, removed at publish.
+__constant__ double2 kSplPE[12] = {
+    {2.5, -1.0}, {1.0, 0.0}, {0.0, 0.0}, {0.0, 0.0},      // s^4,                     s = 2.5 - q
+    {1.5, -1.0}, {-4.0, 4.0}, {6.0, 4.0}, {1.0, 0.0},     // -4s^4+4s^3+6s^2+4s+1,    s = 1.5 - q
+    {0.0, -1.0}, {6.0, 0.0}, {-15.0, 0.0}, {14.375, 0.0}, // 6s^4-15s^2+14.375,       s = -q
 };
 
 __device__ __forceinline__ void density2_stage(D2Tile &T, const ActiveLayout &L, const D2View &jv,
@@ -716,17 +719,18 @@ __device__ __forceinline__ void density2_pair(const FastPolicy::DI &I, const D2T
   const double rinv = fma(y0, e * fma(e, k0375, 0.5), y0);
   const double q = r2 * rinv * I.inv_h;
   const int hq = __double2hiint(q);
-  int row = hq < 0x3FF80000 ? 6 : 0; // q < 1.5
-  if (hq < 0x3FE00000) row = 12;     // q < 0.5
+  int row = hq < 0x3FF80000 ? 4 : 0; // q < 1.5
+  if (hq < 0x3FE00000) row = 8;      // q < 0.5
   const double2 t0 = T.spl[row], t1 = T.spl[row + 1], t2 = T.spl[row + 2];
-  const double2 t3 = T.spl[row + 3], t4 = T.spl[row + 4], t5 = T.spl[row + 5];
+  const double c0 = T.spl[row + 3].x;
   const double sv = fma(t0.y, q, t0.x);
-  const double E = fma(fma(fma(t1.x, sv, t1.y), sv, t2.x), sv, t2.y);
-  const double P = fma(fma(fma(fma(t3.x, sv, t3.y), sv, t4.x), sv, t4.y), sv, t5.x);
+  const double b3 = fma(t1.x, sv, t1.y), b2 = fma(b3, sv, t2.x), b1 = fma(b2, sv, t2.y);
+  const double P = fma(b1, sv, c0);
+  const double D = fma(fma(fma(t1.x, sv, b3), sv, b2), sv, b1); // P'(s) = 4 E
   const double mj = T.m[j];
   s.rho = fma(mj, P, s.rho);
   s.w += P;
-  const double mE = mj * E;
+  const double mE = mj * D; // 4 m E
   s.qe = fma(q, mE, s.qe);
   const double fac = mE * rinv;
   const double2 vj = T.vv[j];
@@ -757,7 +761,7 @@ __global__ void __launch_bounds__(kD2W * 32, MINB) density2_kernel(DenArgs A) {
   const int w = warp_in_cta(), lane = lane_id();
   const int item_idx = blockIdx.x * kD2W + w;
   if (item_idx >= A.n_items) return;
-  if (lane < 18) {
+  if (lane < 12) {
 #pragma unroll
     for (int b = 0; b < 2 + SPH_D2_COMPACT; ++b) tiles[w][b].spl[lane] = kSplPE[lane];
   }
@@ -892,6 +896,9 @@ __global__ void __launch_bounds__(kD2W * 32, MINB) density2_kernel(DenArgs A) {
     }
   }
   if (!live || qs != 0) return;
+  s.qe *= 0.25; // the E sums were accumulated as sums of 4 E (exact scaling)
+  s.div *= 0.25;
+  s.rot *= 0.25;
   double hn = h;
   const int st = FastPolicy::den_step(s, hn, A.target, A.h_max, A.round);
   A.again[it.start + iw] = (unsigned char)(st == 0);
