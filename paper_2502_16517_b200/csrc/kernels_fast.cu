@@ -678,17 +678,18 @@ __global__ void __launch_bounds__(kF2W * 32, MINB) force2_kernel(F2Args A) {
 struct __align__(16) D2Tile {
   double x[kTJ], y[kTJ], m[kTJ];
   double2 vv[kTJ];
-  double2 spl[12]; // rows (outer, mid, inner) x {c_off, sgn}, {c4, c3}, {c2, c1}, {c0, 0}
+  double2 spl[12]; // rows (outer, mid, inner) x {c4, c3}, {c2, c1}, {c_off, c0} (+1 spare)
 };
 
 // W(q) = N P(s) with s = c_off + sgn q (spline.hpp:12-41); the inner piece uses s = -q (P is
 // even there), so on every piece dW/dq = -N dP/ds and the kernel derivative is
 // E = P'(s) / 4, evaluated by the derivative Horner recursion alongside P: four table loads
 // instead of six, the same seven DFMA. Sums over m E carry the factor 4, removed at publish.
+// Rows are 4 entries apart; s = c_off - q on every piece.
 __constant__ double2 kSplPE[12] = {
-    {2.5, -1.0}, {1.0, 0.0}, {0.0, 0.0}, {0.0, 0.0},      // s^4,                     s = 2.5 - q
-    {1.5, -1.0}, {-4.0, 4.0}, {6.0, 4.0}, {1.0, 0.0},     // -4s^4+4s^3+6s^2+4s+1,    s = 1.5 - q
-    {0.0, -1.0}, {6.0, 0.0}, {-15.0, 0.0}, {14.375, 0.0}, // 6s^4-15s^2+14.375,       s = -q
+    {1.0, 0.0}, {0.0, 0.0}, {2.5, 0.0}, {0.0, 0.0},       // s^4,                     s = 2.5 - q
+    {-4.0, 4.0}, {6.0, 4.0}, {1.5, 1.0}, {0.0, 0.0},      // -4s^4+4s^3+6s^2+4s+1,    s = 1.5 - q
+    {6.0, 0.0}, {-15.0, 0.0}, {0.0, 14.375}, {0.0, 0.0},  // 6s^4-15s^2+14.375,       s = -q
 };
 
 __device__ __forceinline__ void density2_stage(D2Tile &T, const ActiveLayout &L, const D2View &jv,
@@ -711,27 +712,29 @@ __device__ __forceinline__ void density2_stage(D2Tile &T, const ActiveLayout &L,
 }
 
 // density_pair (kernels.cpp:97-119) for one in-support pair, on FastPolicy's scaled sums
-__device__ __forceinline__ void density2_pair(const FastPolicy::DI &I, const D2Tile &T, int j,
-                                              double dx, double dy, double r2, double k0375,
-                                              FastPolicy::DA &s) {
+// (the piece comes from r2 against per-i thresholds (0.5h)^2, (1.5h)^2 on the high words,
+// so the coefficient loads issue before the rsqrt chain; a pair within 2^-20 of a knot may
+// take the neighbouring piece, which agrees there to O(dq^3))
+__device__ __forceinline__ void density2_pair(const FastPolicy::DI &I, int hiQ05, int hiQ15,
+                                              const D2Tile &T, int j, double dx, double dy,
+                                              double r2, double k0375, FastPolicy::DA &s) {
+  const int hr = __double2hiint(r2);
+  int row = hr < hiQ15 ? 4 : 0; // q < 1.5
+  if (hr < hiQ05) row = 8;      // q < 0.5
+  const double2 t1 = T.spl[row], t2 = T.spl[row + 1], t3 = T.spl[row + 2];
   const double y0 = rsqrt_seed(r2);
   const double e = fma(-r2, y0 * y0, 1.0);
   const double rinv = fma(y0, e * fma(e, k0375, 0.5), y0);
-  const double q = r2 * rinv * I.inv_h;
-  const int hq = __double2hiint(q);
-  int row = hq < 0x3FF80000 ? 4 : 0; // q < 1.5
-  if (hq < 0x3FE00000) row = 8;      // q < 0.5
-  const double2 t0 = T.spl[row], t1 = T.spl[row + 1], t2 = T.spl[row + 2];
-  const double c0 = T.spl[row + 3].x;
-  const double sv = fma(t0.y, q, t0.x);
+  const double r = r2 * rinv;
+  const double sv = fma(-r, I.inv_h, t3.x); // c_off - q
   const double b3 = fma(t1.x, sv, t1.y), b2 = fma(b3, sv, t2.x), b1 = fma(b2, sv, t2.y);
-  const double P = fma(b1, sv, c0);
+  const double P = fma(b1, sv, t3.y);
   const double D = fma(fma(fma(t1.x, sv, b3), sv, b2), sv, b1); // P'(s) = 4 E
   const double mj = T.m[j];
   s.rho = fma(mj, P, s.rho);
   s.w += P;
   const double mE = mj * D; // 4 m E
-  s.qe = fma(q, mE, s.qe);
+  s.qe = fma(r, mE, s.qe);  // sum r 4 m E = 4 h sum q m E
   const double fac = mE * rinv;
   const double2 vj = T.vv[j];
   const double dvx = I.vx - vj.x, dvy = I.vy - vj.y;
@@ -776,6 +779,7 @@ __global__ void __launch_bounds__(kD2W * 32, MINB) density2_kernel(DenArgs A) {
   const double2 xi = src.x(slot), vi = src.vp(slot);
   const double h = (A.round == 0) ? src.h(slot) : A.hcur[slot];
   const FastPolicy::DI I = FastPolicy::den_i(xi.x, xi.y, vi.x, vi.y, h);
+  const int hiQ05 = __double2hiint(0.25 * h * h), hiQ15 = __double2hiint(2.25 * h * h);
   FastPolicy::DA s = FastPolicy::den_zero();
   const float ixlo = warp_min((float)xi.x), ixhi = warp_max((float)xi.x);
   const float iylo = warp_min((float)xi.y), iyhi = warp_max((float)xi.y);
@@ -861,7 +865,8 @@ __global__ void __launch_bounds__(kD2W * 32, MINB) density2_kernel(DenArgs A) {
           for (int u = 0; u < 4; ++u) r2[u] = fma(dx[u], dx[u], dy[u] * dy[u]);
 #pragma unroll
           for (int u = 0; u < 4; ++u)
-            if (in_support(r2[u], I.hiH2m1)) density2_pair(I, T, j + u, dx[u], dy[u], r2[u], k0375, s);
+            if (in_support(r2[u], I.hiH2m1))
+              density2_pair(I, hiQ05, hiQ15, T, j + u, dx[u], dy[u], r2[u], k0375, s);
         }
       } else {
         constexpr int U = (kTJ / JS) < 4 ? (kTJ / JS) : 4;
@@ -878,7 +883,7 @@ __global__ void __launch_bounds__(kD2W * 32, MINB) density2_kernel(DenArgs A) {
 #pragma unroll
           for (int u = 0; u < U; ++u)
             if (in_support(r2[u], I.hiH2m1))
-              density2_pair(I, T, qs + JS * (t + u), dx[u], dy[u], r2[u], k0375, s);
+              density2_pair(I, hiQ05, hiQ15, T, qs + JS * (t + u), dx[u], dy[u], r2[u], k0375, s);
         }
       }
       __syncwarp();
@@ -896,7 +901,7 @@ __global__ void __launch_bounds__(kD2W * 32, MINB) density2_kernel(DenArgs A) {
     }
   }
   if (!live || qs != 0) return;
-  s.qe *= 0.25; // the E sums were accumulated as sums of 4 E (exact scaling)
+  s.qe *= 0.25 * I.inv_h; // accumulated as sum r (4 m E): to sum q m E
   s.div *= 0.25;
   s.rot *= 0.25;
   double hn = h;
