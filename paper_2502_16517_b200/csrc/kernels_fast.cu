@@ -401,11 +401,22 @@ struct __align__(16) F2Tile {
 
 // spline table rows (outer, mid, inner): {c_off, sgn}, {e3, e2}, {e1, e0};
 // s = c_off + sgn q, E(s) = ((e3 s + e2) s + e1) s + e0 (spline.hpp:12-41 as dW = -4 N E)
+#ifndef SPH_F2_SNEG
+#define SPH_F2_SNEG 1 // s = c_off - q on every piece (inner: s = -q, E = 6 s^3 - 7.5 s)
+#endif
+#if SPH_F2_SNEG
+__constant__ double2 kSplE[9] = {
+    {2.5, -1.0}, {1.0, 0.0}, {0.0, 0.0},   // q in [1.5, 2.5): E = s^3,            s = 2.5 - q
+    {1.5, -1.0}, {-4.0, 3.0}, {3.0, 1.0},  // q in [0.5, 1.5): -4s^3+3s^2+3s+1,    s = 1.5 - q
+    {0.0, -1.0}, {6.0, 0.0}, {-7.5, 0.0},  // q in [0, 0.5):   6s^3 - 7.5s,        s = -q
+};
+#else
 __constant__ double2 kSplE[9] = {
     {2.5, -1.0}, {1.0, 0.0}, {0.0, 0.0},   // q in [1.5, 2.5): E = (2.5 - q)^3
     {1.5, -1.0}, {-4.0, 3.0}, {3.0, 1.0},  // q in [0.5, 1.5): s = 1.5 - q
     {0.0, 1.0}, {-6.0, 0.0}, {7.5, 0.0},   // q in [0, 0.5):   E = -6 q^3 + 7.5 q
 };
+#endif
 
 __device__ __forceinline__ void cp_async8(void *smem, const void *gmem) {
   const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
@@ -467,9 +478,13 @@ __device__ __forceinline__ double force2_sph(const F2I &I, const F2Tile &T, int 
   if (hr < I.hiQ05) row = 6;
   const double c_off = T.spl[row].x;
   const double2 t1 = T.spl[row + 1], t2 = T.spl[row + 2];
+#if SPH_F2_SNEG
+  const double s = fma(-(r2 * rinv), I.inv_hi, c_off);
+#else
   const double sih = __hiloint2double(__double2hiint(I.inv_hi) ^ (row == 6 ? 0 : (int)0x80000000),
                                       __double2loint(I.inv_hi));
   const double s = fma(sih, r2 * rinv, c_off);
+#endif
 #else
   const double q = r2 * rinv * I.inv_hi;
   const int hq = __double2hiint(q);
