@@ -401,6 +401,9 @@ struct __align__(16) F2Tile {
 
 // spline table rows (outer, mid, inner): {c_off, sgn}, {e3, e2}, {e1, e0};
 // s = c_off + sgn q, E(s) = ((e3 s + e2) s + e1) s + e0 (spline.hpp:12-41 as dW = -4 N E)
+#ifndef SPH_F2_ORDER
+#define SPH_F2_ORDER 2 // source order of the SPH block loads (0: as needed, 1: j data first (+3.6 %), 2: table first (-0.3 %))
+#endif
 #ifndef SPH_F2_SNEG
 #define SPH_F2_SNEG 1 // s = c_off - q on every piece (inner: s = -q, E = 6 s^3 - 7.5 s)
 #endif
@@ -465,41 +468,42 @@ struct F2I { double vx, vy, inv_hi, pri, mb3; int hiQ05, hiQ15; };
 __device__ __forceinline__ double force2_sph(const F2I &I, const F2Tile &T, int j, double dx,
                                              double dy, double r2, double k0375, double &udt,
                                              double &hdt, double &vsig) {
-  const double y0 = rsqrt_seed(r2);
-  const double e = fma(-r2, y0 * y0, 1.0);
-  const double rinv = fma(y0, e * fma(e, k0375, 0.5), y0);
-#if SPH_F2_QFREE
-  // piece from r2 against (0.5 h)^2 and (1.5 h)^2 on the high words (a pair within 2^-20
-  // of a knot may take the neighbouring piece: the pieces agree there to O(dq^3), E being
-  // C^2 at the knots); then s = c_off + sgn q = fma(sgn / h, r, c_off). Measured: force
-  // -0.8 %; the same change in density2 was slower (+2 %) and is not used there.
+#if SPH_F2_ORDER == 1
+  const double2 vj = T.vv[j];
+  const double2 cm = T.cm[j], pv = T.pv[j];
+#endif
+#if SPH_F2_ORDER == 2
   const int hr = __double2hiint(r2);
   int row = hr < I.hiQ15 ? 3 : 0;
   if (hr < I.hiQ05) row = 6;
   const double c_off = T.spl[row].x;
   const double2 t1 = T.spl[row + 1], t2 = T.spl[row + 2];
-#if SPH_F2_SNEG
+#endif
+  const double y0 = rsqrt_seed(r2);
+  const double e = fma(-r2, y0 * y0, 1.0);
+  const double rinv = fma(y0, e * fma(e, k0375, 0.5), y0);
+#if SPH_F2_ORDER != 2
+  // piece from r2 against (0.5 h)^2 and (1.5 h)^2 on the high words (a pair within 2^-20
+  // of a knot may take the neighbouring piece: the pieces agree there to O(dq^3), E being
+  // C^2 at the knots); s = c_off - q on every piece
+  const int hr = __double2hiint(r2);
+  int row = hr < I.hiQ15 ? 3 : 0;
+  if (hr < I.hiQ05) row = 6;
+  const double c_off = T.spl[row].x;
+  const double2 t1 = T.spl[row + 1], t2 = T.spl[row + 2];
+#endif
   const double s = fma(-(r2 * rinv), I.inv_hi, c_off);
-#else
-  const double sih = __hiloint2double(__double2hiint(I.inv_hi) ^ (row == 6 ? 0 : (int)0x80000000),
-                                      __double2loint(I.inv_hi));
-  const double s = fma(sih, r2 * rinv, c_off);
-#endif
-#else
-  const double q = r2 * rinv * I.inv_hi;
-  const int hq = __double2hiint(q);
-  int row = hq < 0x3FF80000 ? 3 : 0; // q < 1.5
-  if (hq < 0x3FE00000) row = 6;      // q < 0.5
-  const double2 t0 = T.spl[row], t1 = T.spl[row + 1], t2 = T.spl[row + 2];
-  const double s = fma(t0.y, q, t0.x);
-#endif
   const double E = fma(fma(fma(t1.x, s, t1.y), s, t2.x), s, t2.y);
   const double g = E * rinv;
+#if SPH_F2_ORDER != 1
   const double2 vj = T.vv[j];
+#endif
   const double dvx = I.vx - vj.x, dvy = I.vy - vj.y;
   const double dvdr = fma(dvx, dx, dvy * dy);
   const double gd = g * dvdr;
+#if SPH_F2_ORDER != 1
   const double2 cm = T.cm[j], pv = T.pv[j];
+#endif
   udt = fma(cm.y, gd, udt);
   hdt = fma(pv.y, gd, hdt);
   const double mu = (__double2hiint(dvdr) < 0 ? dvdr : 0.0) * rinv;
