@@ -566,7 +566,7 @@ def main():
     ap.add_argument("--layout", default="resident", choices=["resident", "aos", "convert"])
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--cpu-baseline", type=int, default=1)
-    ap.add_argument("--cpu-sample-pairs", type=float, default=5e9)
+    ap.add_argument("--cpu-sample-pairs", type=float, default=8e9)
     ap.add_argument("--ref-sample-pairs", type=float, default=1.2e9)
     args = ap.parse_args()
     rank, world, local = dist_init()
