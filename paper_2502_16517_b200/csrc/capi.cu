@@ -221,6 +221,7 @@ struct sph_ctx {
   DevBuf<double2> jv2_vv, jv2_pv, jv2_cm;
   int force2 = 1; // FAST force on the resident SoA: issue-lean kernel (env SPH_B200_FORCE2=0: old)
   int den_js0 = 1, den_js1 = 2; // lean density: lanes per particle in round 0 / rounds >= 1
+  double den_dense_frac = 0.35;  // rounds >= 1 use one lane per particle above this pending share
   bool cull = true; // FAST density: spatial j order + chunk culling (env SPH_B200_CULL=0 disables)
   DevBuf<char> dense, cub_tmp;
   PinnedBuf h_stage, h_small;
@@ -438,8 +439,9 @@ struct sph_ctx {
     const int *list = ilist.p;
     const int *cnt_cur = cnt.p; // entries of `list` per cell (round 0: every local)
     int nitems = n_items0;
-    items_a.ensure((size_t)ncells + (size_t)n / (kTI / js1) + 1);
+    items_a.ensure((size_t)ncells + (size_t)n / (kTI / std::max(js0, js1)) + 1);
     items_b.ensure((size_t)ncells + (size_t)n / (kTI / std::max(js0, js1)) + 1);
+    int js_next = js1; // lanes per particle of the next round (adaptive, see below)
     if (js0 > 1) { // round-0 items of 32/js0 particles
       launch_make_items(items_b.p, scalars.p, pairs_dev.p, cnt.p, cell_begin.p, na_cell.p,
                         cell_order.p, ncells, stream, kTI / js0, items_scratch());
@@ -459,7 +461,7 @@ struct sph_ctx {
       A.items = items;
       A.list = list;
       A.round = r;
-      A.jslices = r == 0 ? js0 : js1;
+      A.jslices = r == 0 ? js0 : js_next;
       if (meanw) {
         launch_density_exact(A, nitems, use_aos, true, stream);
         launched();
@@ -471,8 +473,9 @@ struct sph_ctx {
       if (r < 4) CK(cudaEventRecord(rev[2 * r + 1], stream));
       launch_compact_pending(pend_out, cnt_out, list, cnt_cur, again.p, cell_begin.p, ncells,
                              stream);
+      js_next = js1;
       launch_make_items(items_next, scalars.p, pairs_dev.p, cnt_out, cell_begin.p, na_cell.p,
-                        cell_order.p, ncells, stream, kTI / js1, items_scratch());
+                        cell_order.p, ncells, stream, kTI / js_next, items_scratch());
       launched(3);
       pairs_total += pairs;
       max_round = r + 1;
@@ -482,6 +485,19 @@ struct sph_ctx {
       CK(cudaStreamSynchronize(stream));
       nitems = *(int *)h_small.p;
       pairs = *(long long *)((char *)h_small.p + 8);
+      // j-slices pay while the pending particles are sparse (their warps' boxes stay small);
+      // when most of a cell is pending (large n: dt fixed, h small), full warps are compact
+      // already and one lane per particle is faster (2^24: round 1 93.3 -> 91.0 ms; at 2^21,
+      // ~12 % pending, two lanes win: 4.9 -> 4.2 ms)
+      if (js1 > 1 && nitems > 0 && (double)pairs > den_dense_frac * (double)active_pairs) {
+        js_next = 1;
+        launch_make_items(items_next, scalars.p, pairs_dev.p, cnt_out, cell_begin.p, na_cell.p,
+                          cell_order.p, ncells, stream, kTI, items_scratch());
+        launched();
+        CK(cudaMemcpyAsync(h_small.p, scalars.p, sizeof(int), cudaMemcpyDeviceToHost, stream));
+        CK(cudaStreamSynchronize(stream));
+        nitems = *(int *)h_small.p;
+      }
       if (r < 4) {
         float ms = 0;
         CK(cudaEventElapsedTime(&ms, rev[2 * r], rev[2 * r + 1]));
@@ -1147,6 +1163,7 @@ int sph_create(int device, sph_ctx **out) {
   if (const char *e = std::getenv("SPH_B200_PIPELINE")) ctx->pipeline = std::atoi(e);
   if (const char *e = std::getenv("SPH_B200_DEN_JS0")) ctx->den_js0 = std::atoi(e);
   if (const char *e = std::getenv("SPH_B200_DEN_JS1")) ctx->den_js1 = std::atoi(e);
+  if (const char *e = std::getenv("SPH_B200_DEN_DENSE")) ctx->den_dense_frac = std::atof(e);
   int r = guarded(ctx, [&] {
     CK(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
     for (auto &e : ctx->ev) CK(cudaEventCreate(&e));
