@@ -217,8 +217,10 @@ struct sph_ctx {
   DevBuf<unsigned char> rounds, again;
   DevBuf<float4> boxes;
   DevBuf<double2> jv_xy, jv_vv, jv_mg, jv_pv;
-  DevBuf<double> jv_m, jv_c, jv2_x, jv2_y, jv2_gm, jv2_m;
-  DevBuf<double2> jv2_vv, jv2_pv, jv2_cm;
+  DevBuf<double> jv_m, jv_c, jv2_fblk; // jv2_fblk: chunk-major force j-view
+  DevBuf<double> jv2_x, jv2_y, jv2_m;   // density j-view
+  DevBuf<double2> jv2_vv;
+  size_t jv_blocks() const { return (size_t)n / 32 + (size_t)ncells + 2; }
   int force2 = 1; // FAST force on the resident SoA: issue-lean kernel (env SPH_B200_FORCE2=0: old)
   int den_js0 = 1, den_js1 = 2; // lean density: lanes per particle in round 0 / rounds >= 1
   double den_dense_frac = 0.35;  // rounds >= 1 use one lane per particle above this pending share
@@ -284,8 +286,7 @@ struct sph_ctx {
     dd_mask.release(); dd_flag.release(); dd_sel.release(); dd_cnt.release();
     mi_k.release(); mi_off.release(); mi_tmp.release();
     jv_xy.release(); jv_vv.release(); jv_mg.release(); jv_pv.release(); jv_m.release(); jv_c.release();
-    jv2_x.release(); jv2_y.release(); jv2_gm.release(); jv2_vv.release(); jv2_pv.release();
-    jv2_cm.release(); jv2_m.release();
+    jv2_fblk.release(); jv2_x.release(); jv2_y.release(); jv2_m.release(); jv2_vv.release();
   }
 
   Geom geom() const {
@@ -530,8 +531,7 @@ struct sph_ctx {
       // issue-lean kernel (spatial j order, far chunks gravity-only), any layout
       boxes.ensure((size_t)n / 32 + (size_t)ncells + 2);
       launch_chunk_boxes(boxes.p, ilist.p, aos.p, soa, use_aos, cell_begin.p, ncells, stream);
-      jv2_x.ensure(n); jv2_y.ensure(n); jv2_gm.ensure(n);
-      jv2_vv.ensure(n); jv2_pv.ensure(n); jv2_cm.ensure(n);
+      jv2_fblk.ensure(jv_blocks() * kF2Blk);
       F2Args B{};
       B.g = A.g;
       B.items = items0.p;
@@ -540,7 +540,7 @@ struct sph_ctx {
       B.aos = use_aos ? aos.p : nullptr;
       B.soa = soa;
       B.boxes = boxes.p;
-      B.jv = F2View{jv2_x.p, jv2_y.p, jv2_gm.p, jv2_vv.p, jv2_pv.p, jv2_cm.p};
+      B.jv = F2View{jv2_fblk.p};
       launch_force2(B, n_items0, (int)n, stream);
       launched(3);
       stats.force_pairs = active_pairs;
@@ -628,15 +628,14 @@ struct sph_ctx {
     // force prologue: chunk boxes + j-view (main stream)
     boxes.ensure((size_t)n / 32 + (size_t)ncells + 2);
     launch_chunk_boxes(boxes.p, ilist.p, aos.p, soa, false, cell_begin.p, ncells, stream);
-    jv2_x.ensure(n); jv2_y.ensure(n); jv2_gm.ensure(n);
-    jv2_vv.ensure(n); jv2_pv.ensure(n); jv2_cm.ensure(n);
+    jv2_fblk.ensure(jv_blocks() * kF2Blk);
     F2Args A{};
     A.g = geom();
     A.list = ilist.p;
     A.grav = par.grav;
     A.soa = soa;
     A.boxes = boxes.p;
-    A.jv = F2View{jv2_x.p, jv2_y.p, jv2_gm.p, jv2_vv.p, jv2_pv.p, jv2_cm.p};
+    A.jv = F2View{jv2_fblk.p};
     A.items = items_g.p;
     launch_force2(A, 0, (int)n, stream); // j-view only
     launched(2);

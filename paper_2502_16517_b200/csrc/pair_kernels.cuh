@@ -105,11 +105,12 @@ struct ForArgs {
 };
 
 // Issue-lean FAST force (force2_kernel, kernels_fast.cu): j-view split for vector LDS.
+// Chunk-major j-view of the force sweep: block G holds x[32], y[32], grav*m[32],
+// v_pred[32], (P = m p / rho^2, V = m / rho)[32], (c, m)[32] in the tile layout (2304 bytes),
+// padded with inert dummies (x = 1e30, gm = 0).
+constexpr int kF2Blk = 288; // doubles per force block
 struct F2View {
-  const double *x, *y, *gm; // position, grav*m
-  const double2 *vv;        // v_pred
-  const double2 *pv;        // (P = m p / rho^2, V = m / rho)
-  const double2 *cm;        // (c, m)
+  const double *blk;
 };
 
 struct F2Args {

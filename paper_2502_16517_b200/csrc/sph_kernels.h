@@ -18,7 +18,7 @@ void launch_force_fast(const ForArgs &a, int n_items, bool aos, cudaStream_t s);
 // (nx, ny >= 5) and chunk boxes
 void launch_force2(const F2Args &a, int n_items, int n, cudaStream_t s);
 // split j-view for the issue-lean density round (density2_kernel, used by
-// launch_density_fast when DenArgs::jv2.x is set and the mirror is the SoA)
+// launch_density_fast when DenArgs::jv2.x is set)
 struct D2View;
 void launch_jview_density2(const D2View &v, const int *ilist, const Particle *aos,
                            const SoaMirror &f, bool use_aos, int n, cudaStream_t s);
