@@ -401,6 +401,9 @@ struct __align__(16) F2Tile {
 
 // spline table rows (outer, mid, inner): {c_off, sgn}, {e3, e2}, {e1, e0};
 // s = c_off + sgn q, E(s) = ((e3 s + e2) s + e1) s + e0 (spline.hpp:12-41 as dW = -4 N E)
+#ifndef SPH_ONE_SYNC
+#define SPH_ONE_SYNC 1 // one __syncwarp per staged chunk instead of two
+#endif
 #ifndef SPH_F2_EARLYACC
 #define SPH_F2_EARLYACC 1 // measured -0.3 %
 #endif
@@ -586,6 +589,19 @@ __global__ void __launch_bounds__(kF2W * 32, MINB) force2_kernel(F2Args A) {
       todo &= todo - 1;
       const int cnb = __shfl_sync(0xffffffffu, nb, b), ck = __shfl_sync(0xffffffffu, kk, b);
       const bool has_next = todo != 0u;
+#if SPH_ONE_SYNC
+      // one warp barrier per chunk: after it every lane's copies of this chunk are visible
+      // and every lane is done with the previous chunk, whose buffer the next staging reuses
+      if (!staged) force2_stage(tiles[w][buf], L, A.jv, cnb, ck, lane);
+      cp_async_wait<0>();
+      __syncwarp();
+      if (has_next) {
+        const int bn = __ffs(todo) - 1;
+        const int nnb = __shfl_sync(0xffffffffu, nb, bn), nk = __shfl_sync(0xffffffffu, kk, bn);
+        force2_stage(tiles[w][buf ^ 1], L, A.jv, nnb, nk, lane);
+      }
+      staged = has_next;
+#else
       if (!staged) force2_stage(tiles[w][buf], L, A.jv, cnb, ck, lane);
       if (has_next) {
         const int bn = __ffs(todo) - 1;
@@ -597,6 +613,7 @@ __global__ void __launch_bounds__(kF2W * 32, MINB) force2_kernel(F2Args A) {
       }
       staged = has_next;
       __syncwarp();
+#endif
       const F2Tile &T = tiles[w][buf];
       #if SPH_F2_XI_RELOAD
       const double2 xr = src.x(slot);
@@ -672,7 +689,9 @@ __global__ void __launch_bounds__(kF2W * 32, MINB) force2_kernel(F2Args A) {
           }
         }
       }
+#if !SPH_ONE_SYNC
       __syncwarp();
+#endif
       buf ^= 1;
     }
   }
@@ -830,6 +849,17 @@ __global__ void __launch_bounds__(kD2W * 32, MINB) density2_kernel(DenArgs A) {
       todo &= todo - 1;
       const int cnb = __shfl_sync(0xffffffffu, nb, b), ck = __shfl_sync(0xffffffffu, kk, b);
       const bool has_next = todo != 0u;
+#if SPH_ONE_SYNC
+      if (!staged) density2_stage(tiles[w][buf], L, A.jv2, cnb, ck, lane);
+      cp_async_wait<0>();
+      __syncwarp();
+      if (has_next) {
+        const int bn = __ffs(todo) - 1;
+        const int nnb = __shfl_sync(0xffffffffu, nb, bn), nk = __shfl_sync(0xffffffffu, kk, bn);
+        density2_stage(tiles[w][buf ^ 1], L, A.jv2, nnb, nk, lane);
+      }
+      staged = has_next;
+#else
       if (!staged) density2_stage(tiles[w][buf], L, A.jv2, cnb, ck, lane);
       if (has_next) {
         const int bn = __ffs(todo) - 1;
@@ -841,6 +871,7 @@ __global__ void __launch_bounds__(kD2W * 32, MINB) density2_kernel(DenArgs A) {
       }
       staged = has_next;
       __syncwarp();
+#endif
       // per-j culling: a j farther than the warp's reach from the warp box can be in no
       // lane's support (same test as chunk_near, per particle); the others are compacted
       // into tiles[w][2], padded with inert dummies to the pair loop's granule
@@ -911,7 +942,9 @@ __global__ void __launch_bounds__(kD2W * 32, MINB) density2_kernel(DenArgs A) {
               density2_pair(I, hiQ05, hiQ15, T, qs + JS * (t + u), dx[u], dy[u], r2[u], k0375, s);
         }
       }
+#if !SPH_ONE_SYNC
       __syncwarp();
+#endif
       buf ^= 1;
     }
   }
