@@ -241,7 +241,7 @@ def run_decomposed(args, rank, world, local):
 
     ctx = pkg.Context(local, numerics=Numerics[args.numerics.capitalize()],
                       layout=DeviceLayout.Resident)
-    n_glob = args.n * world
+    n_glob = args.n if args.strong else args.n * world
     t0 = time.time()
     par = ctx.make_particles_device(n_glob, args.ppc, args.seed, kind=IC_KIND[args.ic])
     par.dt = args.dt
@@ -284,12 +284,13 @@ def run_decomposed(args, rank, world, local):
     out = {
         "metric": METRIC, "value": workload_pairs / (ms_per_step * 1e-3), "unit": UNIT,
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "higher_is_better": True, "scaling": "strong" if args.strong else "weak",
+        "vs_baseline": None, "dtype": "f64",
         "data": "synthetic: reference make_particles IC of the global box (uniform random 2-D, "
                 "seed 42), generated on each device, byte-identical to the reference",
-        "config": {"workload": f"full SPH step, {args.n} particles per GPU, global box of "
+        "config": {"workload": f"full SPH step, {n_glob // world} particles per GPU, global box of "
                                f"{n_glob} particles (nx={nx}), ppc={args.ppc}, slab decomposition",
-                   "ic": args.ic, "n": n_glob, "n_per_gpu": args.n, "ppc": args.ppc, "nx": nx,
+                   "ic": args.ic, "n": n_glob, "n_per_gpu": n_glob // world, "ppc": args.ppc, "nx": nx,
                    "seed": args.seed, "dt": args.dt, "numerics": args.numerics,
                    "layout": "resident",
                    "l2": "inputs larger than L2 (>= 1 GB of mirrors per GPU)",
@@ -565,6 +566,9 @@ def main():
     ap.add_argument("--ic", default="uniform", choices=["uniform", "clustered"])
     ap.add_argument("--layout", default="resident", choices=["resident", "aos", "convert"])
     ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--strong", action="store_true",
+                    help="N > 1: --particles is the global box (BASELINE config 5 strong scaling) "
+                         "instead of the per-GPU count (weak scaling, the default)")
     ap.add_argument("--cpu-baseline", type=int, default=1)
     ap.add_argument("--cpu-sample-pairs", type=float, default=8e9)
     ap.add_argument("--ref-sample-pairs", type=float, default=1.2e9)
