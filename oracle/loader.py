@@ -76,6 +76,8 @@ class Oracle:
         lib.orc_make_particles.argtypes = [C.c_int64, C.c_int, C.c_uint64, _recp, _f64p, C.c_int]
         lib.orc_pair_stats.argtypes = [_recp, C.c_int, C.c_int, _i64p, _i64p, C.c_void_p, C.c_int,
                                        _i64p]
+        lib.orc_pair_stats_cell.argtypes = [_recp, C.c_int, C.c_int, _i64p, _i64p, C.c_int,
+                                            C.c_int64, C.c_int, _i64p]
         for name in ("orc_drift_one", "orc_kick1_one", "orc_kick2_one"):
             getattr(lib, name).argtypes = [C.c_void_p, _f64p]
         self.lib = lib
@@ -131,6 +133,13 @@ class Oracle:
         m = None if cell_mask is None else np.ascontiguousarray(cell_mask, np.uint8)
         self.lib.orc_pair_stats(recs, nx, ny, cb, li, None if m is None else m.ctypes.data,
                                 threads or self.threads, out)
+        return out
+
+    def pair_stats_cell(self, recs, nx, ny, cb, li, cell, i_stride=1, threads=None) -> np.ndarray:
+        """pair_stats of one cell over every i_stride-th local (threads split the locals)."""
+        out = np.zeros(5, np.int64)
+        self.lib.orc_pair_stats_cell(recs, nx, ny, cb, li, int(cell), int(i_stride),
+                                     threads or self.threads, out)
         return out
 
     def one(self, which: str, rec: np.ndarray, par) -> None:

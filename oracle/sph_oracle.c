@@ -590,3 +590,43 @@ void orc_pair_stats(orc_particle *recs, int nx, int ny, const int64_t *cell_begi
   }
   for (int k = 0; k < 5; ++k) out5[k] = tot[k];
 }
+
+/* orc_pair_stats for one cell c over every i_stride-th local particle, threads splitting the
+ * locals (a bounded sample of a dense cell; the counts are of the sampled pairs). */
+void orc_pair_stats_cell(orc_particle *recs, int nx, int ny, const int64_t *cell_begin,
+                         const int64_t *local_idx, int c, int64_t i_stride, int threads,
+                         int64_t *out5) {
+  grid_t g = {recs, nx, ny, 0.0, cell_begin, local_idx};
+  int64_t cap = max_active(&g);
+  int64_t *act = (int64_t *)malloc(sizeof(int64_t) * (size_t)(cap > 0 ? cap : 1));
+  int64_t na = active_of(&g, c, act);
+  if (i_stride < 1) i_stride = 1;
+  int64_t b = cell_begin[c], nsel = (cell_begin[c + 1] - b + i_stride - 1) / i_stride;
+  int64_t tot[5] = {0, 0, 0, 0, 0};
+#pragma omp parallel num_threads(threads > 0 ? threads : 1)
+  {
+    int64_t loc[5] = {0, 0, 0, 0, 0};
+#pragma omp for schedule(dynamic, 4)
+    for (int64_t k = 0; k < nsel; ++k) {
+      const orc_particle *pi = &recs[local_idx[b + k * i_stride]];
+      double inv_h = 1.0 / pi->h;
+      for (int64_t j = 0; j < na; ++j) {
+        const orc_particle *pj = &recs[act[j]];
+        double dx0 = min_image(pi->x[0] - pj->x[0]);
+        double dx1 = min_image(pi->x[1] - pj->x[1]);
+        double r2 = dx0 * dx0 + dx1 * dx1;
+        loc[0]++;
+        if (r2 <= 0.0) continue;
+        loc[1]++;
+        double q = sqrt(r2) * inv_h;
+        if (q < 2.5) loc[2]++;
+        if (q < 1.5) loc[3]++;
+        if (q < 0.5) loc[4]++;
+      }
+    }
+#pragma omp critical
+    for (int k = 0; k < 5; ++k) tot[k] += loc[k];
+  }
+  free(act);
+  for (int k = 0; k < 5; ++k) out5[k] = tot[k];
+}
