@@ -57,8 +57,8 @@ __device__ __forceinline__ bool in_support(double r2, unsigned hiH2m1) {
 //   q in [1.5, 2.5): s = 2.5 - q, P = s^4,                          E = s^3
 //   q in [0.5, 1.5): s = 1.5 - q, P = -4s^4 + 4s^3 + 6s^2 + 4s + 1, E = -4s^3 + 3s^2 + 3s + 1
 //   q in [0.0, 0.5): s = q,       P = 6s^4 - 15s^2 + 14.375,        E = -6s^3 + 7.5s
-// (SPH_SPLINE3: one Horner with three-way selected coefficients; otherwise the innermost
-// piece is the middle one plus the correction 10 t^4 / 10 t^3, t = 0.5 - q).
+// The innermost
+// piece is the middle one plus the correction 10 t^4 / 10 t^3, t = 0.5 - q.
 // The two outer pieces share Horner evaluation with selected coefficients (c4 == e3,
 // c3 == c1, c0 == e0, e2 == e1), the innermost correction is a rarely-divergent branch.
 struct Spline {
@@ -69,19 +69,6 @@ struct Spline {
     // (1.5 and 0.5 have zero low words), so they run on the ALU pipe
     const int hq = hi_word(q);
     const bool mid = hq < 0x3FF80000;  // q < 1.5
-#if SPH_SPLINE3
-    // three-way coefficient select, local variable s = 2.5 - q | 1.5 - q | q
-    const bool inner = hq < 0x3FE00000; // q < 0.5
-    const double s = inner ? q : (mid ? 1.5 : 2.5) - q;
-    const double e3 = inner ? -6.0 : (mid ? -4.0 : 1.0), e2 = (mid && !inner) ? 3.0 : 0.0;
-    const double e1 = inner ? 7.5 : (mid ? 3.0 : 0.0), e0 = (mid && !inner) ? 1.0 : 0.0;
-    E = fma(fma(fma(e3, s, e2), s, e1), s, e0);
-    if (NEED_P) {
-      const double c4 = inner ? 6.0 : (mid ? -4.0 : 1.0), c31 = (mid && !inner) ? 4.0 : 0.0;
-      const double c2 = inner ? -15.0 : (mid ? 6.0 : 0.0), c0 = inner ? 14.375 : (mid ? 1.0 : 0.0);
-      P = fma(fma(fma(fma(c4, s, c31), s, c2), s, c31), s, c0);
-    }
-#else
     const double s = (mid ? 1.5 : 2.5) - q;
     const double c4 = mid ? -4.0 : 1.0, c31 = mid ? 4.0 : 0.0, c2 = mid ? 6.0 : 0.0;
     const double c0 = mid ? 1.0 : 0.0, e21 = mid ? 3.0 : 0.0;
@@ -92,7 +79,6 @@ struct Spline {
       E = fma(10.0, t3, E);
       if (NEED_P) P = fma(10.0, t3 * t, P);
     }
-#endif
   }
 };
 
@@ -199,15 +185,8 @@ struct FastPolicy {
     o[5] = 4.0 * s.div * n3;
   }
 
-#if SPH_COLD
-  // per-i constants used only on the in-support path and at publish live in shared memory
-  // (one slot per lane), keeping the hot loop's register footprint small
-  struct FCold { double vx, vy, pri, mb3, K, ci, hi, pad; };
-  struct FI { double x, y, inv_hi, eps2; unsigned hiH2m1; FCold *cold; };
-#else
   struct FCold { double pad; };
   struct FI { double x, y, vx, vy, inv_hi, eps2, pri, mb3, ci, hi, K; unsigned hiH2m1; };
-#endif
 
   struct FA { double ax, ay, udt, vsig, hdt, hdt0; };
 
@@ -225,14 +204,8 @@ struct FastPolicy {
     const double adiv = fabs(div_v);
     const double bi = adiv / (adiv + fabs(rot_v) + 0.0001 * c * I.inv_hi);
     const double K = -4.0 * kNorm2d * I.inv_hi * I.inv_hi * I.inv_hi;
-#if SPH_COLD
-    cold->vx = vp.x; cold->vy = vp.y; cold->pri = pri; cold->mb3 = -3.0 * bi; cold->K = K;
-    cold->ci = c; cold->hi = h;
-    I.cold = cold;
-#else
     (void)cold;
     I.vx = vp.x; I.vy = vp.y; I.pri = pri; I.mb3 = -3.0 * bi; I.K = K; I.ci = c; I.hi = h;
-#endif
     return I;
   }
   __device__ static FA for_zero(double h_dt) { return FA{0.0, 0.0, 0.0, -1.0, 0.0, h_dt}; }
@@ -249,11 +222,7 @@ struct FastPolicy {
   __device__ __forceinline__ static double for_in(const FI &I, double dx, double dy, double r2,
                                                   double2 vj, double2 mg, double2 pv, double cj,
                                                   FA &s) {
-#if SPH_COLD
-    const FCold &C = *I.cold;
-#else
     const FI &C = I;
-#endif
     const double rinv = rsqrt_fast(r2);
     const double q = r2 * rinv * I.inv_hi;
     Spline sp;
@@ -296,26 +265,10 @@ struct FastPolicy {
         f[k] = T.mg[j + k].y * rsqrt3_fast(r2[k] + I.eps2);
         in[k] = in_support(r2[k], I.hiH2m1);
       }
-#if SPH_MERGE
-      // one block for the whole group, chains interleaved; pairs outside the support are
-      // evaluated on a safe r2 and their contributions selected away
-      bool any = false;
-#pragma unroll
-      for (int k = 0; k < G; ++k) any |= in[k];
-      if (any) {
-#pragma unroll
-        for (int k = 0; k < G; ++k) {
-          const double add = for_in_masked(I, dx[k], dy[k], in[k] ? r2[k] : 1.0, in[k], T.vv[j + k],
-                                           T.mg[j + k], T.pv[j + k], T.c[j + k], s);
-          f[k] += add;
-        }
-      }
-#else
 #pragma unroll
       for (int k = 0; k < G; ++k)
         if (in[k])
           f[k] += for_in(I, dx[k], dy[k], r2[k], T.vv[j + k], T.mg[j + k], T.pv[j + k], T.c[j + k], s);
-#endif
 #pragma unroll
       for (int k = 0; k < G; ++k) {
         s.ax = fma(-f[k], dx[k], s.ax);
@@ -324,31 +277,6 @@ struct FastPolicy {
     }
   }
 
-  // for_in with the contributions of a pair outside the support selected to zero
-  __device__ __forceinline__ static double for_in_masked(const FI &I, double dx, double dy,
-                                                         double r2, bool in, double2 vj,
-                                                         double2 mg, double2 pv, double cj,
-                                                         FA &s) {
-#if SPH_COLD
-    const FCold &C = *I.cold;
-#else
-    const FI &C = I;
-#endif
-    const double rinv = rsqrt_fast(r2);
-    const double q = r2 * rinv * I.inv_hi;
-    Spline sp;
-    sp.template eval<false>(q);
-    const double g = in ? sp.E * rinv : 0.0;
-    const double dvx = C.vx - vj.x, dvy = C.vy - vj.y;
-    const double dvdr = fma(dvx, dx, dvy * dy);
-    const double gd = g * dvdr;
-    s.udt = fma(mg.x, gd, s.udt);
-    s.hdt = fma(pv.y, gd, s.hdt);
-    const double mu = (hi_word(dvdr) < 0 ? dvdr : 0.0) * rinv;
-    const double vs = fma(mu, C.mb3, cj);
-    if (in && vs > s.vsig) s.vsig = vs;
-    return fma(mg.x, C.pri, pv.x) * g * C.K;
-  }
 
   // Gravity only (chunk out of every lane's support): branch-free, shifted images.
   __device__ static void for_tile_far(const FI &I, const ForTile &T, FA &s) {
@@ -363,11 +291,7 @@ struct FastPolicy {
   }
 
   __device__ static void for_publish(const FI &I, const FA &s, double o[5]) {
-#if SPH_COLD
-    const FCold &C = *I.cold;
-#else
     const FI &C = I;
-#endif
     o[0] = s.ax;
     o[1] = s.ay;
     o[2] = C.pri * C.K * s.udt;
@@ -401,31 +325,11 @@ struct __align__(16) F2Tile {
 
 // spline table rows (outer, mid, inner): {c_off, sgn}, {e3, e2}, {e1, e0};
 // s = c_off + sgn q, E(s) = ((e3 s + e2) s + e1) s + e0 (spline.hpp:12-41 as dW = -4 N E)
-#ifndef SPH_ONE_SYNC
-#define SPH_ONE_SYNC 1 // one __syncwarp per staged chunk instead of two
-#endif
-#ifndef SPH_F2_EARLYACC
-#define SPH_F2_EARLYACC 1 // measured -0.3 %
-#endif
-#ifndef SPH_F2_ORDER
-#define SPH_F2_ORDER 2 // source order of the SPH block loads (0: as needed, 1: j data first (+3.6 %), 2: table first (-0.3 %))
-#endif
-#ifndef SPH_F2_SNEG
-#define SPH_F2_SNEG 1 // s = c_off - q on every piece (inner: s = -q, E = 6 s^3 - 7.5 s)
-#endif
-#if SPH_F2_SNEG
 __constant__ double2 kSplE[9] = {
     {2.5, -1.0}, {1.0, 0.0}, {0.0, 0.0},   // q in [1.5, 2.5): E = s^3,            s = 2.5 - q
     {1.5, -1.0}, {-4.0, 3.0}, {3.0, 1.0},  // q in [0.5, 1.5): -4s^3+3s^2+3s+1,    s = 1.5 - q
     {0.0, -1.0}, {6.0, 0.0}, {-7.5, 0.0},  // q in [0, 0.5):   6s^3 - 7.5s,        s = -q
 };
-#else
-__constant__ double2 kSplE[9] = {
-    {2.5, -1.0}, {1.0, 0.0}, {0.0, 0.0},   // q in [1.5, 2.5): E = (2.5 - q)^3
-    {1.5, -1.0}, {-4.0, 3.0}, {3.0, 1.0},  // q in [0.5, 1.5): s = 1.5 - q
-    {0.0, 1.0}, {-6.0, 0.0}, {7.5, 0.0},   // q in [0, 0.5):   E = -6 q^3 + 7.5 q
-};
-#endif
 
 __device__ __forceinline__ void cp_async8(void *smem, const void *gmem) {
   const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
@@ -464,52 +368,26 @@ constexpr int kF2W = SPH_F2_WPC, kD2W = SPH_D2_WPC;
 
 // SPH part of force_pair (kernels.cpp:132-152) for one in-support pair: accumulates u_dt,
 // h_dt, v_sig and returns the SPH radial factor A*g (the caller applies K).
-#ifndef SPH_F2_XI_RELOAD
-#define SPH_F2_XI_RELOAD 0 // 1: re-read x_i per chunk (L1 hit) instead of keeping it live (measured: noise)
-#endif
-#ifndef SPH_F2_QFREE
-#define SPH_F2_QFREE 1 // spline row from r2 vs per-i thresholds, s = fma(+-1/h, r, c_off)
-#endif
 struct F2I { double vx, vy, inv_hi, pri, mb3; int hiQ05, hiQ15; };
 __device__ __forceinline__ double force2_sph(const F2I &I, const F2Tile &T, int j, double dx,
                                              double dy, double r2, double k0375, double &udt,
                                              double &hdt, double &vsig) {
-#if SPH_F2_ORDER == 1
-  const double2 vj = T.vv[j];
-  const double2 cm = T.cm[j], pv = T.pv[j];
-#endif
-#if SPH_F2_ORDER == 2
   const int hr = __double2hiint(r2);
   int row = hr < I.hiQ15 ? 3 : 0;
   if (hr < I.hiQ05) row = 6;
   const double c_off = T.spl[row].x;
   const double2 t1 = T.spl[row + 1], t2 = T.spl[row + 2];
-#endif
   const double y0 = rsqrt_seed(r2);
   const double e = fma(-r2, y0 * y0, 1.0);
   const double rinv = fma(y0, e * fma(e, k0375, 0.5), y0);
-#if SPH_F2_ORDER != 2
-  // piece from r2 against (0.5 h)^2 and (1.5 h)^2 on the high words (a pair within 2^-20
-  // of a knot may take the neighbouring piece: the pieces agree there to O(dq^3), E being
-  // C^2 at the knots); s = c_off - q on every piece
-  const int hr = __double2hiint(r2);
-  int row = hr < I.hiQ15 ? 3 : 0;
-  if (hr < I.hiQ05) row = 6;
-  const double c_off = T.spl[row].x;
-  const double2 t1 = T.spl[row + 1], t2 = T.spl[row + 2];
-#endif
   const double s = fma(-(r2 * rinv), I.inv_hi, c_off);
   const double E = fma(fma(fma(t1.x, s, t1.y), s, t2.x), s, t2.y);
   const double g = E * rinv;
-#if SPH_F2_ORDER != 1
   const double2 vj = T.vv[j];
-#endif
   const double dvx = I.vx - vj.x, dvy = I.vy - vj.y;
   const double dvdr = fma(dvx, dx, dvy * dy);
   const double gd = g * dvdr;
-#if SPH_F2_ORDER != 1
   const double2 cm = T.cm[j], pv = T.pv[j];
-#endif
   udt = fma(cm.y, gd, udt);
   hdt = fma(pv.y, gd, hdt);
   const double mu = (__double2hiint(dvdr) < 0 ? dvdr : 0.0) * rinv;
@@ -589,7 +467,6 @@ __global__ void __launch_bounds__(kF2W * 32, MINB) force2_kernel(F2Args A) {
       todo &= todo - 1;
       const int cnb = __shfl_sync(0xffffffffu, nb, b), ck = __shfl_sync(0xffffffffu, kk, b);
       const bool has_next = todo != 0u;
-#if SPH_ONE_SYNC
       // one warp barrier per chunk: after it every lane's copies of this chunk are visible
       // and every lane is done with the previous chunk, whose buffer the next staging reuses
       if (!staged) force2_stage(tiles[w][buf], L, A.jv, cnb, ck, lane);
@@ -601,25 +478,8 @@ __global__ void __launch_bounds__(kF2W * 32, MINB) force2_kernel(F2Args A) {
         force2_stage(tiles[w][buf ^ 1], L, A.jv, nnb, nk, lane);
       }
       staged = has_next;
-#else
-      if (!staged) force2_stage(tiles[w][buf], L, A.jv, cnb, ck, lane);
-      if (has_next) {
-        const int bn = __ffs(todo) - 1;
-        const int nnb = __shfl_sync(0xffffffffu, nb, bn), nk = __shfl_sync(0xffffffffu, kk, bn);
-        force2_stage(tiles[w][buf ^ 1], L, A.jv, nnb, nk, lane);
-        cp_async_wait<1>();
-      } else {
-        cp_async_wait<0>();
-      }
-      staged = has_next;
-      __syncwarp();
-#endif
       const F2Tile &T = tiles[w][buf];
-      #if SPH_F2_XI_RELOAD
-      const double2 xr = src.x(slot);
-#else
       const double2 xr = xi;
-#endif
       const double xs = xr.x - L.sx[cnb], ys = xr.y - L.sy[cnb]; // periodic image, i side
       if ((nmask >> b) & 1u) {
 #pragma unroll 1
@@ -639,7 +499,6 @@ __global__ void __launch_bounds__(kF2W * 32, MINB) force2_kernel(F2Args A) {
             f0 = fma(c0, e0 * fma(e0, k1875, 1.5), c0);
             f1 = fma(c1, e1 * fma(e1, k1875, 1.5), c1);
           }
-#if SPH_F2_EARLYACC
           // pair j's acceleration is accumulated before pair j+1's SPH block (fewer live
           // registers inside it); same j order
           if (in_support(r20, hiH2m1))
@@ -650,16 +509,6 @@ __global__ void __launch_bounds__(kF2W * 32, MINB) force2_kernel(F2Args A) {
             f1 = fma(K, force2_sph(I, T, j + 1, dx1, dy1, r21, k0375, udt, hdt, vsig), f1);
           ax = fma(-f1, dx1, ax);
           ay = fma(-f1, dy1, ay);
-#else
-          if (in_support(r20, hiH2m1))
-            f0 = fma(K, force2_sph(I, T, j, dx0, dy0, r20, k0375, udt, hdt, vsig), f0);
-          if (in_support(r21, hiH2m1))
-            f1 = fma(K, force2_sph(I, T, j + 1, dx1, dy1, r21, k0375, udt, hdt, vsig), f1);
-          ax = fma(-f0, dx0, ax);
-          ay = fma(-f0, dy0, ay);
-          ax = fma(-f1, dx1, ax);
-          ay = fma(-f1, dy1, ay);
-#endif
         }
       } else {
 #pragma unroll 1
@@ -689,9 +538,6 @@ __global__ void __launch_bounds__(kF2W * 32, MINB) force2_kernel(F2Args A) {
           }
         }
       }
-#if !SPH_ONE_SYNC
-      __syncwarp();
-#endif
       buf ^= 1;
     }
   }
@@ -795,22 +641,19 @@ __device__ __forceinline__ void density2_pair(const FastPolicy::DI &I, int hiQ05
 // h-iteration rounds >= 1, ~12 % of a cell), so culling and the in-support union stay as
 // tight as in round 0. Lane slice q takes j = q, q + JS, ... of each tile; the JS partial
 // sums are combined with shuffles at the end.
-#ifndef SPH_D2_COMPACT
-#define SPH_D2_COMPACT 1
-#endif
 
 template <int MINB, int JS, bool AOS>
 __global__ void __launch_bounds__(kD2W * 32, MINB) density2_kernel(DenArgs A) {
   // [0], [1]: cp.async staging double buffer; [2]: the staged chunk's j's that can reach
   // the warp (compacted), which the pair loop consumes
-  __shared__ D2Tile tiles[kD2W][2 + SPH_D2_COMPACT];
+  __shared__ D2Tile tiles[kD2W][3];
   __shared__ ActiveLayout lay[kD2W];
   const int w = warp_in_cta(), lane = lane_id();
   const int item_idx = blockIdx.x * kD2W + w;
   if (item_idx >= A.n_items) return;
   if (lane < 12) {
 #pragma unroll
-    for (int b = 0; b < 2 + SPH_D2_COMPACT; ++b) tiles[w][b].spl[lane] = kSplPE[lane];
+    for (int b = 0; b < 3; ++b) tiles[w][b].spl[lane] = kSplPE[lane];
   }
   ActiveLayout &L = lay[w];
   const Item it = A.items[item_idx];
@@ -849,7 +692,6 @@ __global__ void __launch_bounds__(kD2W * 32, MINB) density2_kernel(DenArgs A) {
       todo &= todo - 1;
       const int cnb = __shfl_sync(0xffffffffu, nb, b), ck = __shfl_sync(0xffffffffu, kk, b);
       const bool has_next = todo != 0u;
-#if SPH_ONE_SYNC
       if (!staged) density2_stage(tiles[w][buf], L, A.jv2, cnb, ck, lane);
       cp_async_wait<0>();
       __syncwarp();
@@ -859,25 +701,12 @@ __global__ void __launch_bounds__(kD2W * 32, MINB) density2_kernel(DenArgs A) {
         density2_stage(tiles[w][buf ^ 1], L, A.jv2, nnb, nk, lane);
       }
       staged = has_next;
-#else
-      if (!staged) density2_stage(tiles[w][buf], L, A.jv2, cnb, ck, lane);
-      if (has_next) {
-        const int bn = __ffs(todo) - 1;
-        const int nnb = __shfl_sync(0xffffffffu, nb, bn), nk = __shfl_sync(0xffffffffu, kk, bn);
-        density2_stage(tiles[w][buf ^ 1], L, A.jv2, nnb, nk, lane);
-        cp_async_wait<1>();
-      } else {
-        cp_async_wait<0>();
-      }
-      staged = has_next;
-      __syncwarp();
-#endif
       // per-j culling: a j farther than the warp's reach from the warp box can be in no
       // lane's support (same test as chunk_near, per particle); the others are compacted
       // into tiles[w][2], padded with inert dummies to the pair loop's granule
       int nj = kTJ;
       const D2Tile *Tp = &tiles[w][buf];
-      if constexpr (SPH_D2_COMPACT && JS == 1) { // (rounds >= 1 with j-slices: measured slower)
+      if constexpr (JS == 1) { // (rounds >= 1 with j-slices: measured slower)
         constexpr int PADQ = JS * ((kTJ / JS) < 4 ? (kTJ / JS) : 4); // pair-loop granule
         const D2Tile &S = tiles[w][buf];
         D2Tile &C = tiles[w][2];
@@ -942,9 +771,6 @@ __global__ void __launch_bounds__(kD2W * 32, MINB) density2_kernel(DenArgs A) {
               density2_pair(I, hiQ05, hiQ15, T, qs + JS * (t + u), dx[u], dy[u], r2[u], k0375, s);
         }
       }
-#if !SPH_ONE_SYNC
-      __syncwarp();
-#endif
       buf ^= 1;
     }
   }

@@ -32,15 +32,6 @@ constexpr int kTI = 32;        // local particles per work item (one warp)
 constexpr int kTJ = 32;        // active particles per shared-memory tile
 constexpr int kWarpsPerCta = 4;
 constexpr double kDummyX = 1.0e30;
-#ifndef SPH_SPLINE3
-#define SPH_SPLINE3 0
-#endif
-#ifndef SPH_COLD
-#define SPH_COLD 0 // 1: FAST force keeps in-support-only per-i constants in shared memory (measured slower)
-#endif
-#ifndef SPH_MERGE
-#define SPH_MERGE 0 // 1: FAST force evaluates a pair group's SPH terms in one interleaved block
-#endif
 #ifndef SPH_FJ
 #define SPH_FJ 2 // force: pairs per interleaved gravity group
 #endif
@@ -411,7 +402,6 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, SPH_MINB_FOR) force_kernel(
 
   double2 rx, rv, rmg, rpv;
   double rm, rrho, rp, rc;
-  constexpr bool view = VIEW;
   auto gather = [&](int nb, int k) {
     const int cnt = L.pre[nb + 1] - L.pre[nb];
     const int q = k * kTJ + lane;
