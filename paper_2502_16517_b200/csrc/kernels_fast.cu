@@ -5,8 +5,10 @@
 //   * periodic images are resolved once per stencil cell (shift folded into the staged j
 //     position) instead of d - round(d) per pair (needs nx, ny >= 5, else min image);
 //   * the support test compares the high 32 bits of r^2 and (2.5 h)^2 as integers (ALU
-//     pipe, not FP64 pipe); pairs within 2^-20 of the support edge, where W ~ 1e-23, are
-//     treated as outside. Out-of-support density pairs cost 2 DADD + DMUL + DFMA;
+//     pipe, not FP64 pipe); density pairs within 2^-20 of the support edge, where W ~ 1e-23,
+//     are treated as outside. Force pairs in that band are decided as the reference decides
+//     them (support_cand / ref_support, bit for bit), because the v_sig max is not
+//     continuous at the edge. Out-of-support density pairs cost 2 DADD + DMUL + DFMA;
 //   * sqrt and '/' become rsqrt.approx.f64 (MUFU) + a 2nd-order series correction (~1 ulp);
 //   * the M5 spline is a Horner polynomial in s = 1.5 - q or 2.5 - q with selected
 //     coefficients (no cancellation), plus a rarely-taken correction for q < 0.5;
@@ -51,6 +53,44 @@ __device__ __forceinline__ int hi_word(double v) { return __double2hiint(v); }
 // self pair (r2 == 0) and everything at or beyond the support edge, on the ALU pipe.
 __device__ __forceinline__ bool in_support(double r2, unsigned hiH2m1) {
   return (unsigned)hi_word(r2) - 1u < hiH2m1;
+}
+
+// Force pairs: the v_sig max (kernels.cpp:151) is discontinuous at the support edge (the
+// other pair terms vanish there), so the edge is decided as the reference decides it.
+// support_cand: 3 <= hi(r2) <= hi(H2) + 1 (r2 = 0 and denormal r2 excluded); support_sure:
+// hi(r2) <= hi(H2) - 2, certainly q < 2.5 by any rounding. Candidates in between (a band of
+// ~2^-19 relative width around (2.5 h)^2) take ref_support.
+__device__ __forceinline__ bool support_cand(double r2, unsigned hiH2m1) {
+  return (unsigned)hi_word(r2) - 3u < hiH2m1;
+}
+__device__ __forceinline__ bool support_sure(double r2, unsigned hiH2m1) {
+  return (unsigned)hi_word(r2) < hiH2m1;
+}
+#ifndef SPH_EDGE_INLINE
+#define SPH_EDGE_INLINE __forceinline__
+#endif
+// IEEE sqrt (round to nearest) of a positive normal x without the library's special-case
+// call: y ~ x^-1/2 to ~1 ulp, s = x y, then one residual step s + (x - s^2) y / 2 rounds
+// correctly (tools/sqrt_probe.cu checks it against __dsqrt_rn).
+__device__ __forceinline__ double sqrt_rn_normal(double x) {
+  const double y = rsqrt_fast(x);
+  const double s = __dmul_rn(x, y);
+  const double r = __fma_rn(-s, s, x);
+  return __fma_rn(r, 0.5 * y, s);
+}
+// kernels.cpp:124-136 bit for bit: r2 without contraction, IEEE sqrt, q = r * (1/h) < 2.5
+// (r2 here is within 2^-18 of (2.5 h)^2: positive and normal)
+__device__ SPH_EDGE_INLINE bool ref_support(double dx, double dy, double inv_h) {
+  const double r2 = __dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy));
+  return r2 > 0.0 && __dmul_rn(sqrt_rn_normal(r2), inv_h) < 2.5;
+}
+// ... from the unshifted positions, with the reference's minimum image (kernels.cpp:24)
+__device__ SPH_EDGE_INLINE bool ref_support_xy(double xi0, double xi1, double xj0, double xj1,
+                                            double inv_h) {
+  double d0 = __dsub_rn(xi0, xj0), d1 = __dsub_rn(xi1, xj1);
+  d0 = __dsub_rn(d0, round(d0));
+  d1 = __dsub_rn(d1, round(d1));
+  return ref_support(d0, d1, inv_h);
 }
 
 // M5 spline (spline.hpp:12-41) as W(q) = N P(s), dW/dq = -4 N E(s):
@@ -263,7 +303,11 @@ struct FastPolicy {
         if (MINIMG) { dx[k] -= round(dx[k]); dy[k] -= round(dy[k]); }
         r2[k] = fma(dx[k], dx[k], dy[k] * dy[k]);
         f[k] = T.mg[j + k].y * rsqrt3_fast(r2[k] + I.eps2);
-        in[k] = in_support(r2[k], I.hiH2m1);
+        // edge band: the reference's decision on this (dx, dy) (exact in the minimum-image
+        // mode, where dx is the reference's; with the folded periodic shift dx may differ
+        // from it in the last bit)
+        in[k] = support_cand(r2[k], I.hiH2m1) &&
+                (support_sure(r2[k], I.hiH2m1) || ref_support(dx[k], dy[k], I.inv_hi));
       }
 #pragma unroll
       for (int k = 0; k < G; ++k)
@@ -321,6 +365,8 @@ struct __align__(16) F2Tile {
   double2 vv[kTJ], pv[kTJ], cm[kTJ];
   double2 spl[9]; // spline coefficient table (kSplE), one copy per tile so rows are
                   // addressed relative to the tile pointer
+  double vsig0[kTJ]; // each lane's v_sig before this chunk (force2_edge)
+  int edge;          // nonzero: some lane met an edge-band pair in this chunk (force2_sph)
 };
 
 // spline table rows (outer, mid, inner): {c_off, sgn}, {e3, e2}, {e1, e0};
@@ -369,9 +415,15 @@ constexpr int kF2W = SPH_F2_WPC, kD2W = SPH_D2_WPC;
 // SPH part of force_pair (kernels.cpp:132-152) for one in-support pair: accumulates u_dt,
 // h_dt, v_sig and returns the SPH radial factor A*g (the caller applies K).
 struct F2I { double vx, vy, inv_hi, pri, mb3; int hiQ05, hiQ15; };
+// Candidates include the edge band (support_cand): there the u_dt, h_dt and acceleration
+// terms are O(2^-57) whichever side of q = 2.5 the pair lies, but the v_sig max is not
+// continuous. An edge pair flags the tile (a predicated shared store, no extra register:
+// an extra live register makes ptxas rematerialise the tile address in every block, +5 %);
+// force2_edge then redoes the flagged chunk's v_sig max from the value saved before it,
+// taking edge pairs only where the reference would. The SPH block stays branch-free.
 __device__ __forceinline__ double force2_sph(const F2I &I, const F2Tile &T, int j, double dx,
                                              double dy, double r2, double k0375, double &udt,
-                                             double &hdt, double &vsig) {
+                                             double &hdt, double &vsig, unsigned hiH2m1) {
   const int hr = __double2hiint(r2);
   int row = hr < I.hiQ15 ? 3 : 0;
   if (hr < I.hiQ05) row = 6;
@@ -393,7 +445,29 @@ __device__ __forceinline__ double force2_sph(const F2I &I, const F2Tile &T, int 
   const double mu = (__double2hiint(dvdr) < 0 ? dvdr : 0.0) * rinv;
   const double vs = fma(mu, I.mb3, cm.x);
   if (__double_as_longlong(vs) > __double_as_longlong(vsig)) vsig = vs;
+  if ((unsigned)hr >= hiH2m1) const_cast<F2Tile &>(T).edge = hr;
   return fma(cm.y, I.pri, pv.x) * g;
+}
+
+// A flagged chunk's v_sig max redone from the value before it (kernels.cpp:124-151): the
+// pairs certainly inside with force2_sph's arithmetic, the edge-band pairs only if the
+// reference's support decision, from the unshifted positions, has them inside.
+__device__ __forceinline__ double force2_edge(const F2I &I, const F2Tile &T, int lane, double2 xi,
+                                              double xs, double ys, unsigned hiH2m1) {
+  double vsig = T.vsig0[lane];
+  for (int j = 0; j < kTJ; ++j) {
+    const double dx = xs - T.x[j], dy = ys - T.y[j];
+    const double r2 = fma(dx, dx, dy * dy);
+    if (!support_cand(r2, hiH2m1)) continue;
+    if (!support_sure(r2, hiH2m1) && !ref_support_xy(xi.x, xi.y, T.x[j], T.y[j], I.inv_hi))
+      continue;
+    const double rinv = rsqrt_fast(r2);
+    const double2 vj = T.vv[j];
+    const double dvdr = fma(I.vx - vj.x, dx, (I.vy - vj.y) * dy);
+    const double vs = fma((__double2hiint(dvdr) < 0 ? dvdr : 0.0) * rinv, I.mb3, T.cm[j].x);
+    if (__double_as_longlong(vs) > __double_as_longlong(vsig)) vsig = vs;
+  }
+  return vsig;
 }
 
 __device__ __forceinline__ void force2_stage(F2Tile &T, const ActiveLayout &L, const F2View &jv,
@@ -417,6 +491,7 @@ __global__ void __launch_bounds__(kF2W * 32, MINB) force2_kernel(F2Args A) {
   const int item_idx = blockIdx.x * kF2W + w;
   if (item_idx >= A.n_items) return;
   if (lane < 9) tiles[w][0].spl[lane] = tiles[w][1].spl[lane] = kSplE[lane];
+  if (lane == 0) tiles[w][0].edge = tiles[w][1].edge = 0;
   ActiveLayout &L = lay[w];
   const Item it = A.items[item_idx];
   if (lane == 0) build_active(A.g, it.cell, L);
@@ -482,6 +557,7 @@ __global__ void __launch_bounds__(kF2W * 32, MINB) force2_kernel(F2Args A) {
       const double2 xr = xi;
       const double xs = xr.x - L.sx[cnb], ys = xr.y - L.sy[cnb]; // periodic image, i side
       if ((nmask >> b) & 1u) {
+        tiles[w][buf].vsig0[lane] = vsig;
 #pragma unroll 1
         for (int j = 0; j < kTJ; j += 2) {
           const double2 X = *reinterpret_cast<const double2 *>(&T.x[j]);
@@ -501,14 +577,20 @@ __global__ void __launch_bounds__(kF2W * 32, MINB) force2_kernel(F2Args A) {
           }
           // pair j's acceleration is accumulated before pair j+1's SPH block (fewer live
           // registers inside it); same j order
-          if (in_support(r20, hiH2m1))
-            f0 = fma(K, force2_sph(I, T, j, dx0, dy0, r20, k0375, udt, hdt, vsig), f0);
+          if (support_cand(r20, hiH2m1))
+            f0 = fma(K, force2_sph(I, T, j, dx0, dy0, r20, k0375, udt, hdt, vsig, hiH2m1), f0);
           ax = fma(-f0, dx0, ax);
           ay = fma(-f0, dy0, ay);
-          if (in_support(r21, hiH2m1))
-            f1 = fma(K, force2_sph(I, T, j + 1, dx1, dy1, r21, k0375, udt, hdt, vsig), f1);
+          if (support_cand(r21, hiH2m1))
+            f1 = fma(K, force2_sph(I, T, j + 1, dx1, dy1, r21, k0375, udt, hdt, vsig, hiH2m1), f1);
           ax = fma(-f1, dx1, ax);
           ay = fma(-f1, dy1, ay);
+        }
+        __syncwarp();
+        if (T.edge) { // warp-uniform after the barrier; rare
+          vsig = force2_edge(I, T, lane, xi, xs, ys, hiH2m1);
+          __syncwarp();
+          if (lane == 0) tiles[w][buf].edge = 0;
         }
       } else {
 #pragma unroll 1

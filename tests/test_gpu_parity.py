@@ -425,3 +425,74 @@ def test_fast_full_size_sampled_cells(orc, k):
         bad |= ~e
     limit = max(1, len(sel) // 1000) if k == KernelId.Density else 0
     assert np.count_nonzero(bad) <= limit, f"{np.count_nonzero(bad)} of {len(sel)} outside tolerance"
+
+
+def _hi(v):
+    return int(np.array([v], np.float64).view(np.uint64)[0] >> 32)
+
+
+def _edge_offset(xa, h, inside):
+    """A coordinate xb > xa at which the reference's support test (kernels.cpp:124-136: min
+    image, r2 = dx*dx, q = sqrt(r2) * (1/h)) puts the pair the last representable step inside
+    q = 2.5 (or the first step at or beyond it); r2 then lies in the high-word band of
+    (2.5 h)^2 that the FAST kernel's integer compare cannot decide."""
+    inv_h = 1.0 / h
+
+    def is_in(xb):
+        dx = xa - xb
+        return np.sqrt(dx * dx) * inv_h < 2.5
+
+    xb = xa + 2.5 * h
+    if is_in(xb):
+        while is_in(np.nextafter(xb, np.inf)):
+            xb = np.nextafter(xb, np.inf)
+        last_in = xb
+    else:
+        while not is_in(xb):
+            xb = np.nextafter(xb, -np.inf)
+        last_in = xb
+    return last_in if inside else np.nextafter(last_in, np.inf)
+
+
+def test_force_support_edge_decided_like_reference(orc):
+    """v_sig (kernels.cpp:150-151) is discontinuous at the support edge: a pair a hair
+    inside q = 2.5 enters the max, one a hair outside does not. The FAST force sweep's
+    integer support test cannot tell them apart; the kernel must decide them as the
+    reference does (the issue-lean force2 path: nx >= 5, resident layout)."""
+    h = 0.08
+    a = base_particle(0.5, 0.5)
+    xb = _edge_offset(0.5, h, inside=True)
+    yc = _edge_offset(0.5, h, inside=False)
+    b = base_particle(xb, 0.5)
+    c = base_particle(0.5, yc)
+    for p in (a, b, c):
+        p["h"] = h
+    a["div_v"] = 1.0             # Balsara factor ~1: mu enters v_sig
+    b["v_pred"] = (-1.0, 0.0)    # b approaches a
+    c["v_pred"] = (0.0, -1.0)    # c approaches a too, with a large sound speed
+    b["c"], c["c"] = 5.0, 100.0
+    for p, want_in in ((b, True), (c, False)):
+        d = np.array([0.5 - p["x"][0, 0], 0.5 - p["x"][0, 1]])
+        r2 = d[0] * d[0] + d[1] * d[1]
+        assert (np.sqrt(r2) * (1.0 / h) < 2.5) == want_in
+        assert abs(_hi(r2) - _hi(6.25 * h * h)) <= 1  # inside the undecidable band
+    ring = [(i + 0.5) / 5 for i in range(5)]
+    others = [base_particle(x, y) for x in ring for y in ring
+              if abs(x - 0.5) > 0.3 or abs(y - 0.5) > 0.3]
+    others += [base_particle(0.1, 0.3 + 0.01 * k) for k in range(25 - 3 - len(others))]
+    parts = [a, b, c] + others
+    for k, p in enumerate(parts):
+        p["id"] = k
+    store, grid = _tiny(parts, ppc=1)
+    assert grid.nx == 5
+    par = SphParams(target_wcount=1.0)
+    ref = store.recs.copy()
+    oracle_sweep(orc, KernelId.Force, ref, grid, par)
+    ia = int(np.flatnonzero(ref["id"] == 0)[0])
+    assert 5.0 < ref["v_sig"][ia] < 50.0  # b counted, c not
+    with pkg.Context(0, numerics=Numerics.Fast, layout=DeviceLayout.Resident) as ctx:
+        ctx.bind(grid)
+        ctx.run_sweep(KernelId.Force, par)
+    got = store.recs
+    for f in FOR_FIELDS:
+        assert field_err(got, ref, f).all(), f
