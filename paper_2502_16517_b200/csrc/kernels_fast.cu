@@ -411,6 +411,10 @@ __device__ __forceinline__ int spline_row(double q) {
 #define SPH_D2_WPC 1
 #endif
 constexpr int kF2W = SPH_F2_WPC, kD2W = SPH_D2_WPC;
+#ifndef SPH_F2_FARU
+#define SPH_F2_FARU 2 // far loop unroll (groups of 4 pairs; 2: -0.4 %, 4: same as 2)
+#endif
+constexpr int kF2FarU = SPH_F2_FARU;
 
 // SPH part of force_pair (kernels.cpp:132-152) for one in-support pair: accumulates u_dt,
 // h_dt, v_sig and returns the SPH radial factor A*g (the caller applies K).
@@ -595,7 +599,7 @@ __global__ void __launch_bounds__(kF2W * 32, MINB) force2_kernel(F2Args A) {
           if (lane == 0) tiles[w][buf].edge = 0;
         }
       } else {
-#pragma unroll 1
+#pragma unroll kF2FarU
         for (int j = 0; j < kTJ; j += 4) {
           double dx[4], dy[4], gm[4];
           {
