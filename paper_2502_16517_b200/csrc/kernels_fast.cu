@@ -415,6 +415,14 @@ constexpr int kF2W = SPH_F2_WPC, kD2W = SPH_D2_WPC;
 #define SPH_F2_FARU 2 // far loop unroll (groups of 4 pairs; 2: -0.4 %, 4: same as 2)
 #endif
 constexpr int kF2FarU = SPH_F2_FARU;
+#ifndef SPH_F2_NEARU
+#define SPH_F2_NEARU 4 // near loop unroll (pairs of pairs; measured 2: -0.9 %, 4: -1.9 %, 8: +1.5 %)
+#endif
+constexpr int kF2NearU = SPH_F2_NEARU;
+#ifndef SPH_D2_U
+#define SPH_D2_U 1 // density round-0 pair loop unroll (groups of 4 pairs; 2: +1.5 %)
+#endif
+constexpr int kD2U = SPH_D2_U;
 
 // SPH part of force_pair (kernels.cpp:132-152) for one in-support pair: accumulates u_dt,
 // h_dt, v_sig and returns the SPH radial factor A*g (the caller applies K).
@@ -564,7 +572,7 @@ __global__ void __launch_bounds__(kF2W * 32, MINB) force2_kernel(F2Args A) {
       const double xs = xr.x - L.sx[cnb], ys = xr.y - L.sy[cnb]; // periodic image, i side
       if ((nmask >> b) & 1u) {
         tiles[w][buf].vsig0[lane] = vsig;
-#pragma unroll 1
+#pragma unroll kF2NearU
         for (int j = 0; j < kTJ; j += 2) {
           const double2 X = *reinterpret_cast<const double2 *>(&T.x[j]);
           const double2 Y = *reinterpret_cast<const double2 *>(&T.y[j]);
@@ -823,7 +831,7 @@ __global__ void __launch_bounds__(kD2W * 32, MINB) density2_kernel(DenArgs A) {
       const D2Tile &T = *Tp;
       const double xs = xi.x - L.sx[cnb], ys = xi.y - L.sy[cnb]; // periodic image, i side
       if constexpr (JS == 1) {
-#pragma unroll 1
+#pragma unroll kD2U
         for (int j = 0; j < nj; j += 4) {
           double dx[4], dy[4], r2[4];
           {
