@@ -423,6 +423,10 @@ constexpr int kF2NearU = SPH_F2_NEARU;
 #define SPH_D2_U 1 // density round-0 pair loop unroll (groups of 4 pairs; 2: +1.5 %)
 #endif
 constexpr int kD2U = SPH_D2_U;
+#ifndef SPH_D2_JU
+#define SPH_D2_JU 4 // density j-slice (rounds >= 1) pair loop unroll (4: round 1 -1.4 %)
+#endif
+constexpr int kD2JU = SPH_D2_JU;
 
 // SPH part of force_pair (kernels.cpp:132-152) for one in-support pair: accumulates u_dt,
 // h_dt, v_sig and returns the SPH radial factor A*g (the caller applies K).
@@ -851,7 +855,7 @@ __global__ void __launch_bounds__(kD2W * 32, MINB) density2_kernel(DenArgs A) {
         }
       } else {
         constexpr int U = (kTJ / JS) < 4 ? (kTJ / JS) : 4;
-#pragma unroll 1
+#pragma unroll kD2JU
         for (int t = 0; t * JS < nj; t += U) {
           double dx[U], dy[U], r2[U];
 #pragma unroll
