@@ -19,6 +19,7 @@
 #include <vector>
 
 #include <cub/cub.cuh>
+#include <thrust/iterator/counting_iterator.h>
 
 #include "../../include/sph_b200.h"
 #include "pair_kernels.cuh"
@@ -720,7 +721,7 @@ struct sph_ctx {
     const bool aos_src = !(soa_ahead || soa_valid);
     launch_col_flags(dd_flag.p, aos.p, soa, aos_src, dd_mask.p, (int)n, nx, invert ? 1 : 0, stream);
     size_t tb = 0;
-    cub::CountingInputIterator<int> it(0);
+    thrust::counting_iterator<int> it(0);
     CK(cub::DeviceSelect::Flagged(nullptr, tb, it, dd_flag.p, dd_sel.p, dd_cnt.p, (int)n, stream));
     cub_tmp.ensure(tb);
     CK(cub::DeviceSelect::Flagged(cub_tmp.p, tb, it, dd_flag.p, dd_sel.p, dd_cnt.p, (int)n, stream));
