@@ -66,9 +66,6 @@ __device__ __forceinline__ bool support_cand(double r2, unsigned hiH2m1) {
 __device__ __forceinline__ bool support_sure(double r2, unsigned hiH2m1) {
   return (unsigned)hi_word(r2) < hiH2m1;
 }
-#ifndef SPH_EDGE_INLINE
-#define SPH_EDGE_INLINE __forceinline__
-#endif
 // IEEE sqrt (round to nearest) of a positive normal x without the library's special-case
 // call: y ~ x^-1/2 to ~1 ulp, s = x y, then one residual step s + (x - s^2) y / 2 rounds
 // correctly (tools/sqrt_probe.cu checks it against __dsqrt_rn).
@@ -80,12 +77,12 @@ __device__ __forceinline__ double sqrt_rn_normal(double x) {
 }
 // kernels.cpp:124-136 bit for bit: r2 without contraction, IEEE sqrt, q = r * (1/h) < 2.5
 // (r2 here is within 2^-18 of (2.5 h)^2: positive and normal)
-__device__ SPH_EDGE_INLINE bool ref_support(double dx, double dy, double inv_h) {
+__device__ __forceinline__ bool ref_support(double dx, double dy, double inv_h) {
   const double r2 = __dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy));
   return r2 > 0.0 && __dmul_rn(sqrt_rn_normal(r2), inv_h) < 2.5;
 }
 // ... from the unshifted positions, with the reference's minimum image (kernels.cpp:24)
-__device__ SPH_EDGE_INLINE bool ref_support_xy(double xi0, double xi1, double xj0, double xj1,
+__device__ __forceinline__ bool ref_support_xy(double xi0, double xi1, double xj0, double xj1,
                                             double inv_h) {
   double d0 = __dsub_rn(xi0, xj0), d1 = __dsub_rn(xi1, xj1);
   d0 = __dsub_rn(d0, round(d0));
