@@ -183,6 +183,8 @@ struct sph_ctx {
   cudaStream_t fs[2]{}, post = nullptr, copy = nullptr;
   cudaEvent_t pev[40]{};
   int pipeline = 1; // env SPH_B200_PIPELINE=0: serial force -> kick2 -> download
+  static constexpr int kMaxPipeK = 16;
+  int pipe_k = 16;  // env SPH_B200_PIPE_K: force chunks of the pipelined step (2..16); 16 vs 8: exposed tail 1.57 -> 1.04 ms
   std::string err;
   int numerics = SPH_NUMERICS_FAST;
   int layout = SPH_LAYOUT_FROM_PATH;
@@ -582,7 +584,8 @@ struct sph_ctx {
   // the last force chunk holding one of its particles is through `post`. Times (ms):
   // out[0] force (first chunk start -> last chunk end), out[1] the exposed tail.
   void force_kick2_download_pipelined(void *host, const Params &par, float out[2]) {
-    constexpr int K = 8, G = 64;
+    constexpr int G = 64;
+    const int K = pipe_k; // force chunks (<= kMaxPipeK)
     if (!fs[0]) {
       for (auto &q : fs) CK(cudaStreamCreateWithFlags(&q, cudaStreamNonBlocking));
       // kick2/compaction CTAs must not queue behind the force chunks' CTAs
@@ -607,7 +610,7 @@ struct sph_ctx {
     // K chunks of whole cells with ~equal particle counts
     ChunkBounds B{};
     B.k = K;
-    int kb[K + 1];
+    int kb[kMaxPipeK + 1];
     {
       int c = 0;
       for (int f = 0; f <= K; ++f) {
@@ -1161,6 +1164,8 @@ int sph_create(int device, sph_ctx **out) {
   if (const char *e = std::getenv("SPH_B200_CULL")) ctx->cull = std::atoi(e) != 0;
   if (const char *e = std::getenv("SPH_B200_FORCE2")) ctx->force2 = std::atoi(e);
   if (const char *e = std::getenv("SPH_B200_PIPELINE")) ctx->pipeline = std::atoi(e);
+  if (const char *e = std::getenv("SPH_B200_PIPE_K"))
+    ctx->pipe_k = std::min(sph_ctx::kMaxPipeK, std::max(2, std::atoi(e)));
   if (const char *e = std::getenv("SPH_B200_DEN_JS0")) ctx->den_js0 = std::atoi(e);
   if (const char *e = std::getenv("SPH_B200_DEN_JS1")) ctx->den_js1 = std::atoi(e);
   if (const char *e = std::getenv("SPH_B200_DEN_DENSE")) ctx->den_dense_frac = std::atof(e);

@@ -373,12 +373,14 @@ def test_cpp_dropin_shim_against_reference():
     assert "[shim_parity] passed" in r.stdout
 
 
-def test_step_host_pipelined_equals_serial(monkeypatch):
+@pytest.mark.parametrize("pipe_k", ["3", "16"])
+def test_step_host_pipelined_equals_serial(monkeypatch, pipe_k):
     """The pipelined end-to-end step (force chunks overlapping kick2 and the device->host
     copy of finished records) returns the same bytes as the serial force -> kick2 ->
-    download path: same kernels, same per-particle summation order."""
+    download path: same kernels, same per-particle summation order, for any chunk count."""
     n, ppc, seed = 20000, 256, 5
     out, used = [], []
+    monkeypatch.setenv("SPH_B200_PIPE_K", pipe_k)
     for pipe in ("1", "0"):
         monkeypatch.setenv("SPH_B200_PIPELINE", pipe)
         ctx = pkg.Context(0, numerics=Numerics.Fast, layout=DeviceLayout.Resident)
