@@ -585,7 +585,6 @@ struct sph_ctx {
   // out[0] force (first chunk start -> last chunk end), out[1] the exposed tail.
   void force_kick2_download_pipelined(void *host, const Params &par, float out[2]) {
     constexpr int G = 64;
-    const int K = pipe_k; // force chunks (<= kMaxPipeK)
     if (!fs[0]) {
       for (auto &q : fs) CK(cudaStreamCreateWithFlags(&q, cudaStreamNonBlocking));
       // kick2/compaction CTAs must not queue behind the force chunks' CTAs
@@ -606,8 +605,17 @@ struct sph_ctx {
                        stream));
     CK(cudaStreamSynchronize(stream));
     std::vector<int> kpre(ncells + 1, 0); // items in cells < c
-    for (int c = 0; c < ncells; ++c) kpre[c + 1] = kpre[c] + (cb[c + 1] - cb[c] + kTI - 1) / kTI;
-    // K chunks of whole cells with ~equal particle counts
+    int maxc = 0;
+    for (int c = 0; c < ncells; ++c) {
+      kpre[c + 1] = kpre[c] + (cb[c + 1] - cb[c] + kTI - 1) / kTI;
+      maxc = std::max(maxc, cb[c + 1] - cb[c]);
+    }
+    // chunk count: pipe_k on a near-uniform box; on a variable-ppc box (densest cell > 2x the
+    // mean) at most 8, since chunks of very unequal work leave one of the two force streams
+    // idle (measured, config 3: 16 chunks 150.3 ms vs 8 chunks 146.3 ms end to end)
+    const int K = (double)maxc > 2.0 * n / std::max(1, ncells) ? std::min(pipe_k, 8) : pipe_k;
+    // K chunks of whole cells with ~equal particle counts (equal-work chunks measured worse:
+    // the last chunk's records, whose copy is the exposed tail, grow)
     ChunkBounds B{};
     B.k = K;
     int kb[kMaxPipeK + 1];
