@@ -518,3 +518,32 @@ def test_fast_steps_are_deterministic(orc, ic_kind):
             ctx.download()
         outs.append(recs.tobytes())
     assert outs[0] == outs[1]
+
+
+@pytest.mark.parametrize("swap_at", [1, 270000])
+def test_step_host_non_flat_records(orc, swap_at):
+    """sph_step_host on records that are not one flat array in bound order: the upload
+    verifies the pointer list in slices while copying, and a mismatch (here in the first
+    slice, or in the second after one slice was already queued) falls back to the staged
+    upload. The step's bytes, by particle id, equal those of the flat-array run."""
+    n, ppc, seed = 300000, 1024, 4
+    recs0, par = orc.make_particles(n, ppc, seed)
+    par = SphParams(dt=1e-3, gamma=par.gamma, cfl=par.cfl, grav=par.grav,
+                    target_wcount=par.target_wcount)
+    out = []
+    for swapped in (False, True):
+        recs = recs0.copy()
+        if swapped:  # two storage positions exchanged: the bound pointer list is not flat
+            a, b = swap_at, swap_at + 1000
+            recs[[a, b]] = recs[[b, a]]
+        order = np.argsort(recs["id"], kind="stable").astype(np.int64)
+        store = pkg.ParticleStore(recs, order, pkg.Layout.Scattered if swapped
+                                  else pkg.Layout.Continuous)
+        grid = pkg.build_grid(store, pkg.InitConfig(n=n, ppc=ppc))
+        with pkg.Context(0, numerics=Numerics.Exact, layout=DeviceLayout.Resident) as ctx:
+            ctx.bind(grid)
+            ctx.host_register(recs)
+            ctx.step_host(par)
+            ctx.host_unregister(recs)
+        out.append(recs[np.argsort(recs["id"], kind="stable")].tobytes())
+    assert out[0] == out[1]
