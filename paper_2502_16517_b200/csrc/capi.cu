@@ -621,8 +621,11 @@ struct sph_ctx {
     int kb[kMaxPipeK + 1];
     {
       int c = 0;
+      // the last two chunks are half size: the last chunk's records are the exposed copy
+      const double unit = 1.0 / (K - 1);
       for (int f = 0; f <= K; ++f) {
-        const long long target = (long long)n * f / K;
+        const double frac = std::min(f, K - 2) * unit + std::max(0, f - (K - 2)) * 0.5 * unit;
+        const long long target = (long long)std::llround((double)n * frac);
         while (c < ncells && cb[c] < target) ++c;
         if (f == K) c = ncells;
         B.s[f] = cb[c];
