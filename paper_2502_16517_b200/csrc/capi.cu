@@ -894,9 +894,11 @@ struct sph_ctx {
       dense.ensure(bytes);
       dst = static_cast<char *>(dense.p);
     }
-    constexpr int64_t kSlice = 1 << 18; // records per slice (~71 MB, ~1.3 ms of copy)
-    for (int64_t s = 0; s < n; s += kSlice) {
-      const int64_t e = std::min<int64_t>(n, s + kSlice);
+    // slices of 2^14, 2^16, then 2^18 records (~71 MB, ~1.3 ms of copy): a pointer check
+    // (~1 ns per record) stays ahead of the copy (~5 ns per record) from the second slice on
+    int64_t slice = 1 << 14;
+    for (int64_t s = 0, e; s < n; s = e, slice = std::min<int64_t>(slice * 4, 1 << 18)) {
+      e = std::min<int64_t>(n, s + slice);
       for (int64_t k = s; k < e; ++k)
         if (static_cast<const char *>(recs[k]) != b + k * SPH_RECORD_SIZE) {
           upload_full(recs, 0);
