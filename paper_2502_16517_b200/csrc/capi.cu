@@ -921,8 +921,11 @@ struct sph_ctx {
   void upload_full(void *const *recs, int contig = -1) {
     const size_t bytes = (size_t)n * SPH_RECORD_SIZE;
     if (n == 0) return;
+    if (contig < 0) { // unknown: check while copying
+      upload_full_checked(recs);
+      return;
+    }
     const void *src;
-    if (contig < 0) contig = contiguous(recs);
     if (contig) {
       src = recs[0];
     } else {
@@ -983,16 +986,15 @@ struct sph_ctx {
     if (n == 0) return;
     make_aos_current();
     const size_t bytes = (size_t)n * SPH_RECORD_SIZE;
-    const bool contig = contiguous(recs);
-    void *dst = contig ? recs[0] : (h_stage.ensure(bytes), h_stage.p);
-    if (identity_order) {
-      CK(cudaMemcpyAsync(dst, aos.p, bytes, cudaMemcpyDeviceToHost, stream));
-    } else {
+    if (!identity_order) { // device work first: the host's pointer-list check overlaps it
       dense.ensure(bytes);
       launch_compact(reinterpret_cast<Particle *>(dense.p), aos.p, host_idx.p, (int)n, stream);
       launched();
-      CK(cudaMemcpyAsync(dst, dense.p, bytes, cudaMemcpyDeviceToHost, stream));
     }
+    const bool contig = contiguous(recs);
+    void *dst = contig ? recs[0] : (h_stage.ensure(bytes), h_stage.p);
+    CK(cudaMemcpyAsync(dst, identity_order ? static_cast<void *>(aos.p) : dense.p, bytes,
+                       cudaMemcpyDeviceToHost, stream));
     CK(cudaStreamSynchronize(stream));
     if (!contig) {
       const char *st = static_cast<const char *>(h_stage.p);
