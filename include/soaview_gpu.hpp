@@ -86,11 +86,14 @@ private:
     if (sph_create(device, &ctx_) != SPH_OK || !ctx_)
       throw std::runtime_error("libsph_b200: no usable CUDA device");
   }
+  // Every pointer of every local list, in order: a rebuilt grid at the same address whose
+  // particles swapped cells (or were reordered) behind unchanged list sizes re-binds.
+  // run_sweep walks all n pointers to pack the upload anyway, so this is O(n) of the same.
   static uint64_t signature(const CellGrid &g) {
     uint64_t h = 1469598103934665603ULL ^ static_cast<uint64_t>(g.nx * 131 + g.ny);
     for (const auto &l : g.local) {
       h = (h ^ l.size()) * 1099511628211ULL;
-      h = (h ^ reinterpret_cast<uintptr_t>(l.empty() ? nullptr : l.front())) * 1099511628211ULL;
+      for (const Particle *p : l) h = (h ^ reinterpret_cast<uintptr_t>(p)) * 1099511628211ULL;
     }
     return h;
   }

@@ -132,6 +132,12 @@ int sph_run_sweep(sph_ctx *ctx, int kernel, void *const *recs, const sph_params 
  * kernel_ms (optional, 8 entries): H2D, the six phases, D2H (device time). */
 int sph_step_host(sph_ctx *ctx, void *const *recs, const sph_params *par, double *kernel_ms);
 
+/* drift_one / kick1_one / kick2_one (kernels.hpp:52-54, kernels.cpp:880-893) on n dense host
+ * records (272 B each, in place): copied to a device scratch buffer, updated by the exact
+ * streaming kernel, copied back. Independent of the bound grid. kernel: SPH_DRIFT, SPH_KICK1
+ * or SPH_KICK2. */
+int sph_apply_records(sph_ctx *ctx, int kernel, void *records, int64_t n, const sph_params *par);
+
 /* Page-lock a host range for full-bandwidth copies (cudaHostRegister); optional. */
 int sph_host_register(sph_ctx *ctx, void *base, uint64_t bytes);
 int sph_host_unregister(sph_ctx *ctx, void *base);

@@ -56,6 +56,7 @@ SIGNATURES = {
     "sph_rebin": (C.c_int, [_vp]),
     "sph_step": (C.c_int, [_vp, C.POINTER(SphParamsC), _vp]),
     "sph_step_host": (C.c_int, [_vp, _vp, C.POINTER(SphParamsC), _vp]),
+    "sph_apply_records": (C.c_int, [_vp, C.c_int, _vp, C.c_int64, C.POINTER(SphParamsC)]),
     "sph_host_register": (C.c_int, [_vp, _vp, C.c_uint64]),
     "sph_host_unregister": (C.c_int, [_vp, _vp]),
     "sph_make_particles": (C.c_int, [_vp, C.c_int64, C.c_int, C.c_uint64, C.POINTER(SphParamsC)]),

@@ -198,6 +198,7 @@ struct sph_ctx {
 
   // device state
   DevBuf<Particle> aos, aos_tmp;
+  DevBuf<Particle> lin_recs; // sph_apply_records scratch (independent of the bound mirror)
   DevBuf<double2> f_x, f_v, f_vp, f_a, tmp2;
   DevBuf<double> f_m, f_rho, f_p, f_u, f_upred, f_udt, f_c, f_h, f_wc, f_rdh, f_rot, f_div,
       f_vsig, f_hdt, f_dtn, f_dbg0, tmp1;
@@ -208,7 +209,8 @@ struct sph_ctx {
 
   DevBuf<int> cell_begin, cnt, pend_cnt, pend_cnt2, na_cell, ilist, pend_a, pend_b, host_idx, host_idx_tmp,
       cellnew, vals, vals_sorted, scalars;
-  DevBuf<long long> all_rank, all_rank_tmp, pairs_dev;
+  DevBuf<long long> all_rank, all_rank_tmp, pairs_dev; // pairs_dev: {sum nl*na, particles}
+  DevBuf<unsigned long long> fail_dev; // density: particles that hit the 30-round limit
   DevBuf<unsigned long long> keys, keys_sorted;
   DevBuf<unsigned> cost_key, cost_key_sorted;
   DevBuf<unsigned char> owned;
@@ -247,6 +249,7 @@ struct sph_ctx {
     return &mi;
   }
   int64_t active_pairs = 0;
+  int64_t listed0 = 0; // particles in the round-0 work list (owned cells' locals)
 
   // mirror state
   uint32_t dirty = 0;      // fields written on the device since the last host sync
@@ -271,7 +274,7 @@ struct sph_ctx {
     for (auto &e : rev)
       if (e) cudaEventDestroy(e);
     if (stream) cudaStreamDestroy(stream);
-    aos.release(); aos_tmp.release();
+    aos.release(); aos_tmp.release(); lin_recs.release(); fail_dev.release();
     f_x.release(); f_v.release(); f_vp.release(); f_a.release(); tmp2.release();
     f_m.release(); f_rho.release(); f_p.release(); f_u.release(); f_upred.release();
     f_udt.release(); f_c.release(); f_h.release(); f_wc.release(); f_rdh.release();
@@ -375,11 +378,12 @@ struct sph_ctx {
                       cell_order.p, ncells, stream, kTI, items_scratch());
     launched(3);
     CK(cudaMemcpyAsync(h_small.p, scalars.p, sizeof(int), cudaMemcpyDeviceToHost, stream));
-    CK(cudaMemcpyAsync((char *)h_small.p + 8, pairs_dev.p, sizeof(long long),
+    CK(cudaMemcpyAsync((char *)h_small.p + 8, pairs_dev.p, 2 * sizeof(long long),
                        cudaMemcpyDeviceToHost, stream));
     CK(cudaStreamSynchronize(stream));
     n_items0 = *(int *)h_small.p;
     active_pairs = *(long long *)((char *)h_small.p + 8);
+    listed0 = *(long long *)((char *)h_small.p + 16);
     stats.active_pairs = active_pairs;
   }
 
@@ -456,7 +460,13 @@ struct sph_ctx {
       items = items_b.p;
     }
     int64_t pairs = active_pairs, pairs_total = 0;
+    int64_t pending = listed0, updates = 0;
     int max_round = 0;
+    if (!meanw) {
+      fail_dev.ensure(1);
+      CK(cudaMemsetAsync(fail_dev.p, 0, sizeof(unsigned long long), stream));
+      A.fail_count = fail_dev.p;
+    }
     for (double &v : round_ms) v = 0.0;
     int *pend_out = pend_a.p;
     int *cnt_out = pend_cnt.p;
@@ -482,13 +492,15 @@ struct sph_ctx {
                         cell_order.p, ncells, stream, kTI / js_next, items_scratch());
       launched(3);
       pairs_total += pairs;
+      updates += pending;
       max_round = r + 1;
       CK(cudaMemcpyAsync(h_small.p, scalars.p, sizeof(int), cudaMemcpyDeviceToHost, stream));
-      CK(cudaMemcpyAsync((char *)h_small.p + 8, pairs_dev.p, sizeof(long long),
+      CK(cudaMemcpyAsync((char *)h_small.p + 8, pairs_dev.p, 2 * sizeof(long long),
                          cudaMemcpyDeviceToHost, stream));
       CK(cudaStreamSynchronize(stream));
       nitems = *(int *)h_small.p;
       pairs = *(long long *)((char *)h_small.p + 8);
+      pending = *(long long *)((char *)h_small.p + 16);
       // j-slices pay while the pending particles are sparse (their warps' boxes stay small);
       // when most of a cell is pending (large n: dt fixed, h small), full warps are compact
       // already and one lane per particle is faster (2^24: round 1 93.3 -> 91.0 ms; at 2^21,
@@ -516,7 +528,12 @@ struct sph_ctx {
       cnt_out = (cnt_out == pend_cnt.p) ? pend_cnt2.p : pend_cnt.p;
     }
     if (!meanw) {
+      unsigned long long fails = 0;
+      CK(cudaMemcpyAsync(&fails, fail_dev.p, sizeof fails, cudaMemcpyDeviceToHost, stream));
+      CK(cudaStreamSynchronize(stream));
       stats.density_pairs = pairs_total;
+      stats.density_updates = updates;
+      stats.density_failures = (int64_t)fails;
       stats.density_rounds = max_round;
       for (int k = 0; k < 4; ++k) stats.density_round_ms[k] = round_ms[k];
     }
@@ -1265,7 +1282,10 @@ int sph_set_layout(sph_ctx *ctx, int layout) {
 int sph_bind(sph_ctx *ctx, void *const *recs, const int64_t *cell_begin, int nx, int ny,
              double cell_size, const int64_t *all_rank) {
   return guarded(ctx, [&] {
-    if (!cell_begin || (!recs && cell_begin[(size_t)nx * ny] > 0)) throw ArgError{"null argument"};
+    if (!cell_begin) throw ArgError{"null argument"};
+    if (nx <= 0 || ny <= 0 || (int64_t)nx * ny > (int64_t)INT32_MAX / 2)
+      throw ArgError{"nx and ny must be positive and nx * ny must fit in an int"};
+    if (!recs && cell_begin[(size_t)nx * ny] > 0) throw ArgError{"null argument"};
     ctx->bind(recs, cell_begin, nx, ny, cell_size, all_rank);
     return SPH_OK;
   });
@@ -1464,6 +1484,25 @@ int sph_step_host(sph_ctx *ctx, void *const *recs, const sph_params *par, double
     ctx->stats.last_force_ms = ms[5];
     if (kernel_ms)
       for (int k = 0; k < 8; ++k) kernel_ms[k] = ms[k];
+    return SPH_OK;
+  });
+}
+
+int sph_apply_records(sph_ctx *ctx, int kernel, void *records, int64_t n, const sph_params *par) {
+  return guarded(ctx, [&] {
+    if (kernel != SPH_DRIFT && kernel != SPH_KICK1 && kernel != SPH_KICK2)
+      throw ArgError{"sph_apply_records takes drift, kick1 or kick2"};
+    if (!par || (n > 0 && !records)) throw ArgError{"null argument"};
+    if (n < 0 || n >= (1LL << 31)) throw ArgError{"record count out of range"};
+    if (n == 0) return SPH_OK;
+    const size_t bytes = (size_t)n * SPH_RECORD_SIZE;
+    ctx->lin_recs.ensure((size_t)n);
+    CK(cudaMemcpyAsync(ctx->lin_recs.p, records, bytes, cudaMemcpyHostToDevice, ctx->stream));
+    // the exact streaming kernels on the records in place (AoS); the SoA view is unused
+    launch_linear(kernel, true, ctx->lin_recs.p, SoaMirror{}, (int)n, to_params(par), ctx->stream);
+    ctx->launched();
+    CK(cudaMemcpyAsync(records, ctx->lin_recs.p, bytes, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
     return SPH_OK;
   });
 }

@@ -895,6 +895,7 @@ __global__ void __launch_bounds__(kD2W * 32, MINB) density2_kernel(DenArgs A) {
   double o[6];
   FastPolicy::den_publish(s, h, src.m(slot), o);
   if (A.rounds_out) A.rounds_out[slot] = (unsigned char)(A.round + 1);
+  if (st == 2 && A.fail_count) atomicAdd(A.fail_count, 1ull);
   if constexpr (AOS) {
     Particle &q = const_cast<Particle &>(A.aos[slot]);
     q.h = o[0]; q.rho = o[1]; q.wcount = o[2]; q.rho_dh = o[3]; q.rot_v = o[4]; q.div_v = o[5];

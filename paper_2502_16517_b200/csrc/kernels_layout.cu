@@ -363,7 +363,7 @@ __global__ void __launch_bounds__(1024) make_items_kernel(Item *__restrict__ ite
   __shared__ typename Red::TempStorage tr;
   __shared__ int carry;
   if (threadIdx.x == 0) carry = 0;
-  long long pairs = 0;
+  long long pairs = 0, parts = 0;
   __syncthreads();
   for (int c0 = 0; c0 < ncells; c0 += 1024) {
     const int ci = c0 + threadIdx.x;
@@ -372,6 +372,7 @@ __global__ void __launch_bounds__(1024) make_items_kernel(Item *__restrict__ ite
     if (ci < ncells) {
       k = (cnt[c] + tile - 1) / tile;
       pairs += (long long)cnt[c] * na_cell[c];
+      parts += cnt[c];
     }
     int off, tot;
     Scan(ts).ExclusiveSum(k, off, tot);
@@ -391,9 +392,12 @@ __global__ void __launch_bounds__(1024) make_items_kernel(Item *__restrict__ ite
     __syncthreads();
   }
   long long tp = Red(tr).Sum(pairs);
+  __syncthreads();
+  long long tq = Red(tr).Sum(parts);
   if (threadIdx.x == 0) {
     *n_items_out = carry;
-    *pairs_out = tp;
+    pairs_out[0] = tp;
+    pairs_out[1] = tq;
   }
 }
 
@@ -574,17 +578,22 @@ __global__ void item_counts_kernel(int *__restrict__ k, long long *pairs_out,
                                    const int *__restrict__ cnt, const int *__restrict__ na_cell,
                                    const int *__restrict__ order, int ncells, int tile) {
   typedef cub::BlockReduce<long long, 256> Red;
-  __shared__ typename Red::TempStorage tr;
+  __shared__ typename Red::TempStorage tr, tq;
   const int ci = blockIdx.x * blockDim.x + threadIdx.x;
-  long long p = 0;
+  long long p = 0, q = 0;
   if (ci < ncells) {
     const int c = order ? order[ci] : ci;
     k[ci] = (cnt[c] + tile - 1) / tile;
     p = (long long)cnt[c] * na_cell[c];
+    q = cnt[c];
   }
   const long long tot = Red(tr).Sum(p);
+  const long long totq = Red(tq).Sum(q);
+  // pairs_out[0]: sum of nl * na over the listed particles; pairs_out[1]: their count
   if (threadIdx.x == 0 && tot) atomicAdd(reinterpret_cast<unsigned long long *>(pairs_out),
                                          (unsigned long long)tot);
+  if (threadIdx.x == 0 && totq) atomicAdd(reinterpret_cast<unsigned long long *>(pairs_out + 1),
+                                          (unsigned long long)totq);
 }
 __global__ void item_write_kernel(Item *__restrict__ items, int *n_items_out,
                                   const int *__restrict__ off, const int *__restrict__ k,
@@ -613,7 +622,7 @@ void launch_make_items(Item *items, int *n_items_out, long long *pairs_out, cons
                                          order, ncells, tile);
     return;
   }
-  cudaMemsetAsync(pairs_out, 0, sizeof(long long), s);
+  cudaMemsetAsync(pairs_out, 0, 2 * sizeof(long long), s);
   const int g = (ncells + 255) / 256;
   item_counts_kernel<<<g, 256, 0, s>>>(scr->k, pairs_out, cnt, na_cell, order, ncells, tile);
   size_t tb = scr->tmp_bytes;

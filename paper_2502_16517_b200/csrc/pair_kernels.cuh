@@ -80,6 +80,8 @@ struct DenArgs {
   D2View jv2;           // issue-lean FAST sweep (resident SoA): split j-view (x null = off)
   double k0375;         // series constant (kernel parameter -> constant-bank operand)
   int jslices;          // density2: lanes per local particle (1, 2, 4); items hold 32/jslices
+  unsigned long long *fail_count; // optional: particles that hit the 30-round limit
+                                  // (density_step's Fail, kernels.cpp:190), for sph_stats
 };
 
 struct ForArgs {
@@ -278,6 +280,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, SPH_MINB_DEN) density_round
   double o[6]; // h, rho, wcount, rho_dh, rot_v, div_v
   P::den_publish(s, h, mi, o);
   if (A.rounds_out) A.rounds_out[slot] = (unsigned char)(A.round + 1);
+  if (st == 2 && A.fail_count) atomicAdd(A.fail_count, 1ull);
   if constexpr (AOS) {
     Particle &q = const_cast<Particle &>(A.aos[slot]);
     q.h = o[0]; q.rho = o[1]; q.wcount = o[2]; q.rho_dh = o[3]; q.rot_v = o[4]; q.div_v = o[5];
@@ -555,6 +558,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, SPH_MINB_DEN) density_cull_
   double o[6];
   P::den_publish(s, h, mi, o);
   if (A.rounds_out) A.rounds_out[slot] = (unsigned char)(A.round + 1);
+  if (st == 2 && A.fail_count) atomicAdd(A.fail_count, 1ull);
   if constexpr (AOS) {
     Particle &pq = const_cast<Particle &>(A.aos[slot]);
     pq.h = o[0]; pq.rho = o[1]; pq.wcount = o[2]; pq.rho_dh = o[3]; pq.rot_v = o[4]; pq.div_v = o[5];

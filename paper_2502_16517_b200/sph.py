@@ -394,20 +394,17 @@ def run_sweep(k: KernelId, grid: CellGrid, par: SphParams, path: Path = Path.Aos
     return ctx.run_sweep(k, par, path, order, guard)
 
 
-# Single-particle ops (kernels.hpp:52-54) run as a one-particle sweep on the device.
+# Single-particle ops (kernels.hpp:52-54): the exact streaming kernel on the device over the
+# given records (sph_apply_records), without touching the context's bound grid.
 def _one(kernel: KernelId, rec: np.ndarray, par: SphParams, ctx: Context | None) -> None:
-    """``rec``: a one-element PARTICLE_DTYPE array (e.g. ``recs[i:i+1]``), updated in place."""
+    """``rec``: a contiguous PARTICLE_DTYPE array (one record, e.g. ``recs[i:i+1]``, or
+    several), updated in place."""
     ctx = ctx or default_context()
-    one = np.asarray(rec)
-    if one.dtype != PARTICLE_DTYPE or one.size != 1 or not one.flags.c_contiguous:
-        raise ValueError("expected a contiguous one-element PARTICLE_DTYPE array view")
-    one = one.reshape(1)
-    store = ParticleStore(one, np.zeros(1, np.int64), Layout.Continuous)
-    grid = CellGrid(1, 1, 1.0, np.array([0, 1], np.int64), np.zeros(1, np.int64), store,
-                    all_rank=np.zeros(1, np.int64))
-    ctx.bind(grid)
-    ctx.run_sweep(kernel, par)
-    ctx.grid = None
+    arr = np.asarray(rec)
+    if arr.dtype != PARTICLE_DTYPE or not arr.flags.c_contiguous or not arr.flags.writeable:
+        raise ValueError("expected a contiguous, writeable PARTICLE_DTYPE array view")
+    _check(ctx.h, ctx.lib.sph_apply_records(ctx.h, int(kernel), arr.ctypes.data, arr.size,
+                                            C.byref(_cpar(par))), "sph_apply_records")
 
 
 def drift_one(rec: np.ndarray, par: SphParams, ctx: Context | None = None) -> None:
