@@ -16,8 +16,9 @@ SPH steps/s is reported beside it.
            copies all records host->device and device->host (pinned host memory)
   roofline: force kernel (largest share of the step) vs the FP64 pipe peak measured
            live by a DFMA microbenchmark (sph_fp64_peak); HBM kernels beside it
-  cpu_baseline: the unmodified reference (oracle/_ref) on this host's cores, one step on
-           a bounded sample of cells scaled by pair count (oracle/ref_bench.py)
+  cpu_baseline: the unmodified reference (oracle/_ref) on this host's cores, one full step
+           from the same state (oracle/ref_bench.py)
+  --impl reference: the same reference, full steps, nothing of this repo's CUDA loaded
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 N>1 (torchrun): weak scaling, --particles per GPU of one global box slab-decomposed
@@ -211,11 +212,11 @@ def pair_fractions(store, grid, ncells_sample=64, seed=1, pairs_per_cell=2e8):
     return tuple(float(np.dot(k, [f[i] for f in fr]) / k.sum()) for i in (1, 2, 3))
 
 
-def config_block(args, grid, world):
+def config_block(args, nx, world):
     box = ("uniform 2-D box" if args.ic == "uniform" else
            "clustered 2-D box (variable ppc: half uniform, half in 16 Gaussian clumps)")
     return {"workload": f"full SPH step, {box}, n={args.n}, ppc={args.ppc}", "ic": args.ic,
-            "n": args.n, "ppc": args.ppc, "nx": grid.nx if grid else None, "seed": args.seed,
+            "n": args.n, "ppc": args.ppc, "nx": nx, "seed": args.seed,
             "dt": args.dt, "numerics": args.numerics, "layout": args.layout,
             "l2": (f"inputs larger than L2 (AoS mirror {272 * args.n / 1e9:.2f} GB + SoA mirror "
                    f"~{210 * args.n / 1e9:.2f} GB)"),
@@ -404,7 +405,7 @@ def run_replicas(args, rank, world, local):
         "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic: reference make_particles IC (uniform random 2-D, seed 42), "
                 "generated on device, byte-identical to the reference",
-        "config": config_block(args, grid, world),
+        "config": config_block(args, grid.nx, world),
         "steps_per_s": 1e3 / ms_per_step * world,
         "workload_pairs_per_step": workload_pairs,
         "density_pairs_evaluated_per_step": den_eval / args.steps,
@@ -502,58 +503,84 @@ def _host_state(ctx, store):
 
 
 def cpu_baseline(ctx, store, grid, par, args):
+    """One full reference step (oracle/_ref) from the device's current state, on all host
+    cores, wall clock; rank 0 at N = 1 only."""
     from oracle.ref_bench import ReferenceStepper
     st = _host_state(ctx, store)
     stepper = ReferenceStepper(st.recs, args.ppc, par.as_array(), sample_pairs=args.cpu_sample_pairs)
     t = stepper.step()
+    frac = t["sample_fraction"]
+    what = ("density and force on every cell" if frac >= 1.0 else
+            f"density and force on {100 * frac:.1f}% of the pair work, random cells, scaled by "
+            f"pair count")
     return {"value": t["workload_pairs"] / t["step"], "unit": UNIT,
             "cores": stepper.threads, "kind": "reference",
             "step_seconds": t["step"], "measured_seconds": t["measured_seconds"],
-            "sample": f"one reference step (kick1, drift, build_grid, kick2 on all {args.n} "
-                      f"particles; density and force on {100 * t['sample_fraction']:.1f}% of the "
-                      f"pair work, random cells, scaled by pair count) of the same workload "
-                      f"state; oracle/_ref built from /root/reference; wall clock",
+            "sample": f"one full reference step (kick1, drift, build_grid, kick2 on all {args.n} "
+                      f"particles; {what}) of the same workload state; oracle/_ref built from "
+                      f"/root/reference; wall clock",
             "phase_seconds": {k: round(t[k], 4) for k in
                               ("kick1", "drift", "rebin", "density", "force", "kick2")}}
 
 
+def _loaded_native_libs():
+    """Shared objects of this repo mapped into the process (for the reference arm's
+    self-check: it must not load libsph_b200.so)."""
+    try:
+        with open("/proc/self/maps") as f:
+            paths = {ln.split()[-1] for ln in f if ln.rstrip().endswith(".so")}
+    except OSError:
+        return []
+    return sorted(os.path.relpath(p, ROOT) for p in paths if p.startswith(ROOT))
+
+
 def run_reference(args, rank, world, local):
-    """The reference's own CPU implementation (oracle/_ref) on this host's cores."""
+    """The reference's own CPU implementation (oracle/_ref, the unmodified reference sources
+    compiled by oracle/Makefile) on this host's cores: full steps (kick1, drift, build_grid,
+    density, force, kick2 through the reference's run_sweep / build_grid on every cell),
+    wall clock. Nothing of this repo's CUDA library is loaded on this arm."""
     if rank != 0:
         return None
-    import paper_2502_16517_b200 as pkg
-    from oracle import ref_available
+    from oracle import Oracle, ref_available
     from oracle.ref_bench import ReferenceStepper
     if not ref_available():
         return {"impl": "reference", "unavailable": "oracle/_ref was not built (needs /root/reference)"}
-    # IC: identical bytes to reference make_particles (which needs ~4 min on 8 cores at
-    # 2^21); produced by the device IC path, outside the timed region.
-    with pkg.Context(local) as ctx:
-        store, grid, par = ctx.make_particles(args.n, args.ppc, args.seed, kind=IC_KIND[args.ic])
+    # IC: the reference make_particles (grid.cpp:76-143) as restated by oracle/liboracle.so,
+    # threaded and byte-identical to the reference's own (tests/test_oracle.py); the
+    # reference's single-threaded make_particles needs ~4 min at 2^21. Outside the timed region.
+    t0 = time.time()
+    recs, par = Oracle().make_particles(args.n, args.ppc, args.seed, kind=IC_KIND[args.ic])
+    t_ic = time.time() - t0
     par.dt = args.dt
-    stepper = ReferenceStepper(store.recs, args.ppc, par.as_array(),
-                               sample_pairs=args.ref_sample_pairs)
+    stepper = ReferenceStepper(recs, args.ppc, par.as_array(), sample_pairs=args.ref_sample_pairs)
     for _ in range(args.warmup):
         stepper.step()
     ts = [stepper.step() for _ in range(args.steps)]
     step_s = float(np.mean([t["step"] for t in ts]))
     pairs = ts[0]["workload_pairs"]
     v = pairs / step_s
+    frac = ts[0]["sample_fraction"]
+    sample = ("each step: the full reference step (kick1, drift, build_grid, density, force, "
+              "kick2) on every cell and particle" if frac >= 1.0 else
+              f"each step: linear kernels + build_grid on all particles, density/force on "
+              f"{100 * frac:.1f}% of the pair work (random cells), scaled by pair count")
+    libs = _loaded_native_libs()
+    assert not any("libsph_b200" in p for p in libs), libs
     return {
         "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_s * 1e3,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic: reference make_particles IC (uniform random 2-D, seed 42)",
-        "config": config_block(args, grid, 1),
+        "config": config_block(args, grid_nx(args.n, args.ppc), 1),
         "steps_per_s": 1.0 / step_s,
         "workload_pairs_per_step": pairs,
         "phase_seconds": {k: round(float(np.mean([t[k] for t in ts])), 4)
                           for k in ("kick1", "drift", "rebin", "density", "force", "kick2")},
         "cpu_baseline": {"value": v, "unit": UNIT, "cores": stepper.threads, "kind": "reference",
-                         "sample": f"each step: linear kernels + build_grid on all particles, "
-                                   f"density/force on {100 * ts[0]['sample_fraction']:.1f}% of "
-                                   f"the pair work (random cells), scaled by pair count"},
+                         "sample": sample},
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "ic_seconds": round(t_ic, 2),
+        "native_libs_loaded": libs,
         "gpu_launches": 0,
     }
 
@@ -577,8 +604,11 @@ def main():
                     help="N > 1: --particles is the global box (BASELINE config 5 strong scaling) "
                          "instead of the per-GPU count (weak scaling, the default)")
     ap.add_argument("--cpu-baseline", type=int, default=1)
-    ap.add_argument("--cpu-sample-pairs", type=float, default=8e9)
-    ap.add_argument("--ref-sample-pairs", type=float, default=1.2e9)
+    ap.add_argument("--cpu-sample-pairs", type=float, default=None,
+                    help="cpu_baseline: restrict density/force to ~x pairs of random cells "
+                         "(default: the full reference step)")
+    ap.add_argument("--ref-sample-pairs", type=float, default=None,
+                    help="--impl reference: as --cpu-sample-pairs (default: full steps)")
     args = ap.parse_args()
     rank, world, local = dist_init()
     if args.impl == "reference":

@@ -1,12 +1,15 @@
-"""CPU timing of the UNMODIFIED reference on a bounded sample of the bench workload.
+"""CPU timing of the UNMODIFIED reference on the bench workload.
 
 Used only by bench.py's cpu_baseline leg and its ``--impl reference`` arm (test/baseline
 infrastructure; never on the product path). One reference "step" mirrors the GPU step:
 kick1 -> drift -> build_grid -> density -> force -> kick2 through the reference's own
-run_sweep / build_grid (oracle/_ref, compiled from /root/reference). The linear kernels
-and build_grid run on every particle; density and force run on a random sample of cells
-(run_sweep skips cells whose local list is empty, kernels.cpp:548) and are scaled to the
-full workload by pair count, so a step costs a few seconds instead of ~110 s at 2^21.
+run_sweep / build_grid (oracle/_ref, compiled from /root/reference), every kernel on every
+cell (``sample_pairs=None``, the default: a full step, ~30 s at 2^21 on 16 cores).
+
+``sample_pairs=x`` restricts density and force to random cells holding ~x pairs
+(run_sweep skips cells whose local list is empty, kernels.cpp:548) and scales by pair
+count. That is only for quick looks: unsampled cells never get their h updated, so later
+sampled steps take extra h-rounds and the estimate is biased high.
 Times are wall clock around each call (KernelTimes sums per-thread CPU time,
 kernels.cpp:526-531).
 """
@@ -39,7 +42,7 @@ def stencil_pairs(cb: np.ndarray, nx: int, ny: int) -> np.ndarray:
 
 class ReferenceStepper:
     def __init__(self, recs: np.ndarray, ppc: int, par, threads: int | None = None,
-                 sample_pairs: float = 1.2e9, seed: int = 0):
+                 sample_pairs: float | None = None, seed: int = 0):
         self.ref = RefLib()
         self.recs = recs
         self.ppc = ppc
@@ -65,12 +68,14 @@ class ReferenceStepper:
         cb, _ = g.local_csr()
         per_cell = stencil_pairs(cb, g.nx, g.ny)
         total = int(per_cell.sum())
-        frac = min(1.0, self.sample_pairs / max(total, 1))
-        mask = self.rng.random(g.nx * g.ny) < frac
-        if not mask.any():
-            mask[self.rng.integers(g.nx * g.ny)] = True
-        sample = int(per_cell[mask].sum())
-        g.keep_cells(mask.astype(np.uint8))
+        if self.sample_pairs is None or self.sample_pairs >= total:
+            sample = total  # the full step: every cell
+        else:
+            mask = self.rng.random(g.nx * g.ny) < self.sample_pairs / max(total, 1)
+            if not mask.any():
+                mask[self.rng.integers(g.nx * g.ny)] = True
+            sample = int(per_cell[mask].sum())
+            g.keep_cells(mask.astype(np.uint8))
         t0 = time.perf_counter()
         g.run_sweep(0, par, threads=th)  # density (sampled cells)
         t_den = time.perf_counter() - t0
