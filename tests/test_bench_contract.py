@@ -56,3 +56,16 @@ def test_bench_decomposed_two_ranks_on_one_gpu():
     assert "slab decomposition" in d["config"]["parallelism"]
     assert d["config"]["n"] == 2 * 65536
     assert d["exchange_bytes_per_step_rank0"] > 0
+
+
+def test_reference_arm_is_the_reference_on_cpu(ref):
+    """--impl reference: full reference steps (every cell), nothing of libsph_b200 loaded."""
+    out = subprocess.run([sys.executable, "bench.py", "--impl", "reference", "--particles", "20000",
+                          "--ppc", "64", "--steps", "2", "--warmup", "1"],
+                         cwd=ROOT, capture_output=True, text=True, timeout=600, check=True).stdout
+    d = _last_json(out)
+    assert d["impl"] == "reference" and d["value"] > 0
+    assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["gpu_launches"] == 0
+    assert "every cell" in d["cpu_baseline"]["sample"]
+    assert not any("libsph_b200" in p for p in d["native_libs_loaded"])
+    assert "oracle/_ref/libsoaview_ref.so" in d["native_libs_loaded"]
