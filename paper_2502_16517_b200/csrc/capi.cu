@@ -204,6 +204,17 @@ struct sph_ctx {
       f_vsig, f_hdt, f_dtn, f_dbg0, tmp1;
   DevBuf<int32_t> f_frozen, f_moved;
   DevBuf<int64_t> f_flags, tmp8;
+  // rebin by fix-up: the second SoA set the fused permute writes into (swapped in after)
+  DevBuf<double2> g_x, g_v, g_vp, g_a;
+  DevBuf<double> g_m, g_rho, g_p, g_u, g_upred, g_udt, g_c, g_h, g_wc, g_rdh, g_rot, g_div,
+      g_vsig, g_hdt, g_dtn, g_dbg0;
+  DevBuf<int32_t> g_frozen, g_moved;
+  DevBuf<int64_t> g_flags;
+  DevBuf<int> slot_cell, slot_cell_tmp, fx_moved, fx_mpos, fx_out, fx_in, fx_in_begin, fx_in_fill,
+      fx_inlist, fx_new_begin, fx_perm;
+  DevBuf<char> fx_scan;
+  bool fixup_ok = false;   // slots in (cell, all_rank) order with slot_cell current (rebin_fixup)
+  int rebin_fixup_on = 1;  // env SPH_B200_REBIN_FIXUP=0: every rebin sorts
   bool soa_alloc = false;
   SoaMirror soa{};
 
@@ -293,6 +304,14 @@ struct sph_ctx {
     mi_k.release(); mi_off.release(); mi_tmp.release();
     jv_xy.release(); jv_vv.release(); jv_mg.release(); jv_pv.release(); jv_m.release(); jv_c.release();
     jv2_fblk.release(); jv2_x.release(); jv2_y.release(); jv2_m.release(); jv2_vv.release();
+    g_x.release(); g_v.release(); g_vp.release(); g_a.release(); g_m.release(); g_rho.release();
+    g_p.release(); g_u.release(); g_upred.release(); g_udt.release(); g_c.release(); g_h.release();
+    g_wc.release(); g_rdh.release(); g_rot.release(); g_div.release(); g_vsig.release();
+    g_hdt.release(); g_dtn.release(); g_dbg0.release(); g_frozen.release(); g_moved.release();
+    g_flags.release(); slot_cell.release(); slot_cell_tmp.release(); fx_moved.release();
+    fx_mpos.release(); fx_out.release(); fx_in.release(); fx_in_begin.release();
+    fx_in_fill.release(); fx_inlist.release(); fx_new_begin.release(); fx_perm.release();
+    fx_scan.release();
   }
 
   Geom geom() const {
@@ -785,6 +804,7 @@ struct sph_ctx {
     if (keep == n) return;
     apply_perm(dd_sel.p, keep); // (sel is read before the buffers it indexes are swapped)
     n = keep;
+    fixup_ok = false;
     dd_reset_host_order();
     need_rebin = true;
     CK(cudaStreamSynchronize(stream));
@@ -806,6 +826,7 @@ struct sph_ctx {
     std::swap(all_rank.cap, all_rank_tmp.cap);
     CK(cudaStreamSynchronize(stream));
     n = nn;
+    fixup_ok = false;
     alloc_for(n, ncells); // scratch sized for the new count (aos / all_rank already are)
     soa_valid = false;    // the SoA is re-gathered from the AoS by the next resident sweep
     soa_ahead = false;
@@ -1045,6 +1066,7 @@ struct sph_ctx {
     soa_valid = false;
     soa_ahead = false;
     identity_order = true;
+    fixup_ok = false; // the first rebin sorts (the caller's in-cell order is not assumed)
     CK(cudaMemcpyAsync(cell_begin.p, cb.data(), sizeof(int) * (nc + 1), cudaMemcpyHostToDevice, stream));
     std::vector<int> hid(std::max<int64_t>(n, 1));
     std::vector<long long> ar(std::max<int64_t>(n, 1));
@@ -1124,9 +1146,83 @@ struct sph_ctx {
     }
   }
 
+  // build_grid (grid.cpp:145-184) after a drift, by fix-up: the slots are already in
+  // (cell, all_rank) order from the last rebin, only the movers change cell and the stayers
+  // keep their order, so the new order is a per-cell merge (kernels_layout.cu fixup_*), and
+  // every per-slot array moves in one fused pass. Same result as the sort, byte for byte.
+  void rebin_fixup() {
+    const int N = (int)n;
+    slot_cell_tmp.ensure(n); fx_moved.ensure(n + 1); fx_mpos.ensure(n + 1); fx_inlist.ensure(n);
+    fx_perm.ensure(n); cellnew.ensure(n);
+    fx_out.ensure(ncells); fx_in.ensure(ncells); fx_in_begin.ensure(ncells);
+    fx_in_fill.ensure(ncells); fx_new_begin.ensure(ncells + 1);
+    const size_t sb = fixup_scan_bytes(N);
+    fx_scan.ensure(sb);
+    FixupArgs F{};
+    F.n = N; F.ncells = ncells; F.nx = nx; F.ny = ny;
+    F.aos = aos.p; F.soa = soa; F.aos_src = !soa_ahead;
+    F.slot_cell = slot_cell.p; F.cell_begin = cell_begin.p; F.all_rank = all_rank.p;
+    F.cellnew = cellnew.p; F.moved = fx_moved.p; F.mpos = fx_mpos.p; F.out_cnt = fx_out.p;
+    F.in_cnt = fx_in.p; F.in_begin = fx_in_begin.p; F.in_fill = fx_in_fill.p;
+    F.inlist = fx_inlist.p; F.new_begin = fx_new_begin.p; F.perm = fx_perm.p;
+    F.scan_tmp = fx_scan.p; F.scan_bytes = sb;
+    launch_rebin_fixup(F, stream);
+    launched(6);
+    const bool soa_data = soa_valid || soa_ahead;
+    SoaMirror dst{};
+    if (soa_data) {
+      const size_t M = (size_t)n;
+      g_x.ensure(M); g_v.ensure(M); g_vp.ensure(M); g_a.ensure(M); g_m.ensure(M);
+      g_rho.ensure(M); g_p.ensure(M); g_u.ensure(M); g_upred.ensure(M); g_udt.ensure(M);
+      g_c.ensure(M); g_h.ensure(M); g_wc.ensure(M); g_rdh.ensure(M); g_rot.ensure(M);
+      g_div.ensure(M); g_vsig.ensure(M); g_hdt.ensure(M); g_dtn.ensure(M); g_dbg0.ensure(M);
+      g_frozen.ensure(M); g_moved.ensure(M); g_flags.ensure(M);
+      dst = SoaMirror{g_x.p, g_v.p, g_vp.p, g_a.p, g_m.p, g_rho.p, g_p.p, g_u.p, g_upred.p,
+                      g_udt.p, g_c.p, g_h.p, g_wc.p, g_rdh.p, g_rot.p, g_div.p, g_vsig.p,
+                      g_hdt.p, g_dtn.p, g_dbg0.p, g_frozen.p, g_moved.p, g_flags.p};
+    }
+    host_idx_tmp.ensure(n);
+    all_rank_tmp.ensure(n);
+    aos_tmp.ensure(n);
+    // resident (SoA ahead): only the record fields without a SoA array move with the SoA;
+    // otherwise whole records, then p->cell
+    launch_permute_fused(fx_perm.p, N, soa, dst, soa_data, host_idx.p, host_idx_tmp.p,
+                         all_rank.p, all_rank_tmp.p, cellnew.p, slot_cell_tmp.p, aos.p,
+                         soa_ahead ? aos_tmp.p : nullptr, stream);
+    launched();
+    if (!soa_ahead) {
+      launch_permute<Particle>(aos_tmp.p, aos.p, fx_perm.p, N, stream);
+      launched();
+    }
+    auto sw = [](auto &a, auto &b) { std::swap(a.p, b.p); std::swap(a.cap, b.cap); };
+    sw(aos, aos_tmp); sw(host_idx, host_idx_tmp); sw(all_rank, all_rank_tmp);
+    sw(slot_cell, slot_cell_tmp); sw(cell_begin, fx_new_begin);
+    if (soa_data) {
+      sw(f_x, g_x); sw(f_v, g_v); sw(f_vp, g_vp); sw(f_a, g_a); sw(f_m, g_m); sw(f_rho, g_rho);
+      sw(f_p, g_p); sw(f_u, g_u); sw(f_upred, g_upred); sw(f_udt, g_udt); sw(f_c, g_c);
+      sw(f_h, g_h); sw(f_wc, g_wc); sw(f_rdh, g_rdh); sw(f_rot, g_rot); sw(f_div, g_div);
+      sw(f_vsig, g_vsig); sw(f_hdt, g_hdt); sw(f_dtn, g_dtn); sw(f_dbg0, g_dbg0);
+      sw(f_frozen, g_frozen); sw(f_moved, g_moved); sw(f_flags, g_flags);
+      soa = SoaMirror{f_x.p, f_v.p, f_vp.p, f_a.p, f_m.p, f_rho.p, f_p.p, f_u.p, f_upred.p,
+                      f_udt.p, f_c.p, f_h.p, f_wc.p, f_rdh.p, f_rot.p, f_div.p, f_vsig.p,
+                      f_hdt.p, f_dtn.p, f_dbg0.p, f_frozen.p, f_moved.p, f_flags.p};
+    }
+    if (!soa_ahead) {
+      launch_set_cell(aos.p, cell_begin.p, ncells, stream); // build_grid writes p->cell
+      launched();
+    }
+    dirty |= F_CELL;
+    identity_order = false;
+    rebuild_worklist();
+  }
+
   void rebin() {
     if (n == 0) return;
     need_rebin = false;
+    if (fixup_ok && rebin_fixup_on) {
+      rebin_fixup();
+      return;
+    }
     const bool soa_src = soa_ahead;
     keys.ensure(n); keys_sorted.ensure(n); vals.ensure(n); vals_sorted.ensure(n); cellnew.ensure(n);
     launch_rebin_keys(keys.p, vals.p, cellnew.p, aos.p, soa, !soa_src, all_rank.p, (int)n, nx, ny, stream);
@@ -1144,7 +1240,10 @@ struct sph_ctx {
     launch_cell_begin_from_sorted(cell_begin.p, keys_sorted.p, (int)n, ncells, stream);
     apply_perm(perm, n);
     launch_set_cell(aos.p, cell_begin.p, ncells, stream); // build_grid writes p->cell (grid.cpp:156)
-    launched();
+    slot_cell.ensure(n);
+    launch_slot_cell_from_keys(slot_cell.p, keys_sorted.p, (int)n, stream);
+    launched(2);
+    fixup_ok = true;
     dirty |= F_CELL;
     identity_order = false;
     rebuild_worklist();
@@ -1232,6 +1331,7 @@ int sph_create(int device, sph_ctx **out) {
   if (!ctx) return SPH_E_CUDA;
   ctx->device = device;
   if (const char *e = std::getenv("SPH_B200_CULL")) ctx->cull = std::atoi(e) != 0;
+  if (const char *e = std::getenv("SPH_B200_REBIN_FIXUP")) ctx->rebin_fixup_on = std::atoi(e);
   if (const char *e = std::getenv("SPH_B200_FORCE2")) ctx->force2 = std::atoi(e);
   if (const char *e = std::getenv("SPH_B200_PIPELINE")) ctx->pipeline = std::atoi(e);
   if (const char *e = std::getenv("SPH_B200_PIPE_K"))

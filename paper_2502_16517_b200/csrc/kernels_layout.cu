@@ -464,6 +464,160 @@ __global__ void set_cell_kernel(Particle *aos, const int *cell_begin, int ncells
     aos[s].cell = c;
 }
 
+
+// ---- rebin by fix-up (sph_ctx::rebin_fixup) ----
+// Slots are in (cell, all_rank) order (build_grid's list order, grid.cpp:152-158). After a
+// drift only the movers (new cell != slot's cell, ~1e-3 of the particles per step) change
+// cell, and the stayers keep their relative order, so the new order is a merge: per cell,
+// the stayers in slot order interleaved by all_rank with the movers that arrive.
+__device__ __forceinline__ int cell_of_x(double2 x, int nx, int ny) {
+  // grid.cpp:153-155 (clamp_cell(floor(x * nx)))
+  const int cx = min(max((int)floor(x.x * nx), 0), nx - 1);
+  const int cy = min(max((int)floor(x.y * nx), 0), ny - 1);
+  return cy * nx + cx;
+}
+
+__global__ void fixup_flags_kernel(int *__restrict__ cellnew, int *__restrict__ moved,
+                                   int *__restrict__ out_cnt, int *__restrict__ in_cnt,
+                                   const Particle *__restrict__ aos, SoaMirror f, bool aos_src,
+                                   const int *__restrict__ slot_cell, int n, int nx, int ny) {
+  const int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s > n) return;
+  if (s == n) { // sentinel: moved[n] = 0 so the exclusive scan's entry n is the total
+    moved[n] = 0;
+    return;
+  }
+  const double2 x = aos_src ? *reinterpret_cast<const double2 *>(aos[s].x) : f.x[s];
+  const int c = cell_of_x(x, nx, ny), c0 = slot_cell[s];
+  cellnew[s] = c;
+  moved[s] = c != c0;
+  if (c != c0) {
+    atomicAdd(&out_cnt[c0], 1);
+    atomicAdd(&in_cnt[c], 1);
+  }
+}
+
+// One block: new_begin = exclusive scan of (old count - out + in), in_begin = exclusive scan
+// of in; in_fill zeroed.
+__global__ void __launch_bounds__(1024) fixup_cells_kernel(int *__restrict__ new_begin,
+                                                           int *__restrict__ in_begin,
+                                                           int *__restrict__ in_fill,
+                                                           const int *__restrict__ cell_begin,
+                                                           const int *__restrict__ out_cnt,
+                                                           const int *__restrict__ in_cnt,
+                                                           int ncells) {
+  typedef cub::BlockScan<int2, 1024> Scan;
+  __shared__ typename Scan::TempStorage ts;
+  const int per = (ncells + 1023) / 1024;
+  const int b = threadIdx.x * per, e = min(ncells, b + per);
+  int2 acc = make_int2(0, 0);
+  for (int c = b; c < e; ++c) {
+    acc.x += cell_begin[c + 1] - cell_begin[c] - out_cnt[c] + in_cnt[c];
+    acc.y += in_cnt[c];
+  }
+  int2 pre;
+  struct Add2 {
+    __device__ int2 operator()(int2 a, int2 b) const { return make_int2(a.x + b.x, a.y + b.y); }
+  };
+  Scan(ts).ExclusiveScan(acc, pre, make_int2(0, 0), Add2());
+  for (int c = b; c < e; ++c) {
+    new_begin[c] = pre.x;
+    in_begin[c] = pre.y;
+    in_fill[c] = 0;
+    pre.x += cell_begin[c + 1] - cell_begin[c] - out_cnt[c] + in_cnt[c];
+    pre.y += in_cnt[c];
+  }
+  if (threadIdx.x == 1023) new_begin[ncells] = cell_begin[ncells]; // the count is conserved
+}
+
+__global__ void fixup_inlist_kernel(int *__restrict__ inlist, int *__restrict__ in_fill,
+                                    const int *__restrict__ moved, const int *__restrict__ cellnew,
+                                    const int *__restrict__ in_begin, int n) {
+  const int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= n || !moved[s]) return;
+  const int c = cellnew[s];
+  inlist[in_begin[c] + atomicAdd(&in_fill[c], 1)] = s;
+}
+
+// New slot of every particle (perm[new] = old).
+__global__ void fixup_newslot_kernel(int *__restrict__ perm, const int *__restrict__ moved,
+                                     const int *__restrict__ cellnew,
+                                     const int *__restrict__ slot_cell,
+                                     const int *__restrict__ cell_begin,
+                                     const int *__restrict__ new_begin,
+                                     const int *__restrict__ mpos, const int *__restrict__ in_begin,
+                                     const int *__restrict__ in_cnt, const int *__restrict__ inlist,
+                                     const long long *__restrict__ all_rank, int n) {
+  const int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= n) return;
+  const long long r = all_rank[s];
+  int ns;
+  if (!moved[s]) {
+    const int c = slot_cell[s], ob = cell_begin[c];
+    int ins = 0;
+    for (int k = in_begin[c], e = k + in_cnt[c]; k < e; ++k) ins += all_rank[inlist[k]] < r;
+    ns = new_begin[c] + (s - ob) - (mpos[s] - mpos[ob]) + ins;
+  } else {
+    const int c = cellnew[s], ob = cell_begin[c];
+    int lo = ob, hi = cell_begin[c + 1]; // first old slot of c with all_rank > r
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if (all_rank[mid] < r) lo = mid + 1; else hi = mid;
+    }
+    int ins = 0;
+    for (int k = in_begin[c], e = k + in_cnt[c]; k < e; ++k) ins += all_rank[inlist[k]] < r;
+    ns = new_begin[c] + (lo - ob) - (mpos[lo] - mpos[ob]) + ins;
+  }
+  perm[ns] = s;
+}
+
+// Every per-slot array in one pass: dst[k] = src[perm[k]] for the SoA mirror (when it holds
+// data), host_idx, all_rank, the slot's cell, and (TAILS) the record fields without a SoA
+// array (id, cell := the new cell, dbg[1], spare), i.e. build_grid's p->cell write
+// (grid.cpp:156) fused into the move.
+template <bool SOA, bool TAILS>
+__global__ void permute_fused_kernel(const int *__restrict__ perm, int n, SoaMirror src,
+                                     SoaMirror dst, const int *__restrict__ hid_src,
+                                     int *__restrict__ hid_dst, const long long *__restrict__ ar_src,
+                                     long long *__restrict__ ar_dst, const int *__restrict__ cellnew,
+                                     int *__restrict__ slot_cell, const Particle *__restrict__ rsrc,
+                                     Particle *__restrict__ rdst) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  const int s = perm[k];
+  const int c = cellnew[s];
+  slot_cell[k] = c;
+  hid_dst[k] = hid_src[s];
+  ar_dst[k] = ar_src[s];
+  if (SOA) {
+    dst.x[k] = src.x[s]; dst.v[k] = src.v[s]; dst.vp[k] = src.vp[s]; dst.a[k] = src.a[s];
+    dst.m[k] = src.m[s]; dst.rho[k] = src.rho[s]; dst.p[k] = src.p[s]; dst.u[k] = src.u[s];
+    dst.u_pred[k] = src.u_pred[s]; dst.u_dt[k] = src.u_dt[s]; dst.c[k] = src.c[s];
+    dst.h[k] = src.h[s]; dst.wcount[k] = src.wcount[s]; dst.rho_dh[k] = src.rho_dh[s];
+    dst.rot_v[k] = src.rot_v[s]; dst.div_v[k] = src.div_v[s]; dst.v_sig[k] = src.v_sig[s];
+    dst.h_dt[k] = src.h_dt[s]; dst.dt_next[k] = src.dt_next[s]; dst.dbg0[k] = src.dbg0[s];
+    dst.frozen[k] = src.frozen[s]; dst.moved[k] = src.moved[s]; dst.flags[k] = src.flags[s];
+  }
+  if (TAILS) {
+    const uint4 *a = reinterpret_cast<const uint4 *>(rsrc + s);
+    uint4 *b = reinterpret_cast<uint4 *>(rdst + k);
+    uint4 t = a[12]; // id (192), cell (200)
+    const long long cl = c;
+    t.z = (unsigned)cl;
+    t.w = (unsigned)(cl >> 32);
+    b[12] = t;
+    b[14] = a[14]; // dbg[1] (224), spare[0] (232)
+    b[15] = a[15];
+    b[16] = a[16];
+  }
+}
+
+__global__ void slot_cell_from_keys_kernel(int *__restrict__ slot_cell,
+                                           const unsigned long long *__restrict__ keys, int n) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k < n) slot_cell[k] = (int)(keys[k] >> 40);
+}
+
 __global__ void fp64_probe_kernel(double *out, int iters) {
   double a0 = threadIdx.x * 1e-9, a1 = a0 + 1e-9, a2 = a0 + 2e-9, a3 = a0 + 3e-9;
   double a4 = a0 + 4e-9, a5 = a0 + 5e-9, a6 = a0 + 6e-9, a7 = a0 + 7e-9;
@@ -705,6 +859,49 @@ void launch_permute_record_tails(Particle *dst, const Particle *src, const int *
 }
 void launch_set_cell(Particle *aos, const int *cell_begin, int ncells, cudaStream_t s) {
   if (ncells > 0) set_cell_kernel<<<ncells, 128, 0, s>>>(aos, cell_begin, ncells);
+}
+
+size_t fixup_scan_bytes(int n) {
+  size_t tb = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, tb, (const int *)nullptr, (int *)nullptr, n + 1);
+  return tb;
+}
+void launch_rebin_fixup(const FixupArgs &a, cudaStream_t s) {
+  const int n = a.n;
+  cudaMemsetAsync(a.out_cnt, 0, sizeof(int) * a.ncells, s);
+  cudaMemsetAsync(a.in_cnt, 0, sizeof(int) * a.ncells, s);
+  fixup_flags_kernel<<<(n + 1 + 255) / 256, 256, 0, s>>>(a.cellnew, a.moved, a.out_cnt, a.in_cnt,
+                                                          a.aos, a.soa, a.aos_src, a.slot_cell, n,
+                                                          a.nx, a.ny);
+  size_t tb = a.scan_bytes;
+  cub::DeviceScan::ExclusiveSum(a.scan_tmp, tb, a.moved, a.mpos, n + 1, s);
+  fixup_cells_kernel<<<1, 1024, 0, s>>>(a.new_begin, a.in_begin, a.in_fill, a.cell_begin,
+                                        a.out_cnt, a.in_cnt, a.ncells);
+  fixup_inlist_kernel<<<(n + 255) / 256, 256, 0, s>>>(a.inlist, a.in_fill, a.moved, a.cellnew,
+                                                      a.in_begin, n);
+  fixup_newslot_kernel<<<(n + 255) / 256, 256, 0, s>>>(a.perm, a.moved, a.cellnew, a.slot_cell,
+                                                       a.cell_begin, a.new_begin, a.mpos,
+                                                       a.in_begin, a.in_cnt, a.inlist, a.all_rank,
+                                                       n);
+}
+void launch_permute_fused(const int *perm, int n, const SoaMirror &src, const SoaMirror &dst,
+                          bool soa, const int *hid_src, int *hid_dst, const long long *ar_src,
+                          long long *ar_dst, const int *cellnew, int *slot_cell,
+                          const Particle *rsrc, Particle *rdst, cudaStream_t s) {
+  if (n <= 0) return;
+  const int g = (n + 255) / 256;
+  if (soa && rdst)
+    permute_fused_kernel<true, true><<<g, 256, 0, s>>>(perm, n, src, dst, hid_src, hid_dst, ar_src, ar_dst, cellnew, slot_cell, rsrc, rdst);
+  else if (soa)
+    permute_fused_kernel<true, false><<<g, 256, 0, s>>>(perm, n, src, dst, hid_src, hid_dst, ar_src, ar_dst, cellnew, slot_cell, rsrc, rdst);
+  else if (rdst)
+    permute_fused_kernel<false, true><<<g, 256, 0, s>>>(perm, n, src, dst, hid_src, hid_dst, ar_src, ar_dst, cellnew, slot_cell, rsrc, rdst);
+  else
+    permute_fused_kernel<false, false><<<g, 256, 0, s>>>(perm, n, src, dst, hid_src, hid_dst, ar_src, ar_dst, cellnew, slot_cell, rsrc, rdst);
+}
+void launch_slot_cell_from_keys(int *slot_cell, const unsigned long long *keys, int n,
+                                cudaStream_t s) {
+  if (n > 0) slot_cell_from_keys_kernel<<<(n + 255) / 256, 256, 0, s>>>(slot_cell, keys, n);
 }
 void launch_fp64_probe(double *out, int blocks, int iters, cudaStream_t s) {
   fp64_probe_kernel<<<blocks, 256, 0, s>>>(out, iters);

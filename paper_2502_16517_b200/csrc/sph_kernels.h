@@ -108,6 +108,28 @@ void launch_permute(T *dst, const T *src, const int *perm, int n, cudaStream_t s
 void launch_permute_record_tails(Particle *dst, const Particle *src, const int *perm, int n,
                                  cudaStream_t s);
 void launch_set_cell(Particle *aos, const int *cell_begin, int ncells, cudaStream_t s);
+// rebin by fix-up (capi.cu sph_ctx::rebin_fixup): movers only, merge order
+struct FixupArgs {
+  int n, ncells, nx, ny;
+  const Particle *aos;
+  SoaMirror soa;
+  bool aos_src;
+  const int *slot_cell, *cell_begin;
+  const long long *all_rank;
+  int *cellnew, *moved, *mpos, *out_cnt, *in_cnt, *in_begin, *in_fill, *inlist, *new_begin, *perm;
+  void *scan_tmp;
+  size_t scan_bytes;
+};
+size_t fixup_scan_bytes(int n);
+void launch_rebin_fixup(const FixupArgs &a, cudaStream_t s);
+// dst[k] = src[perm[k]] for the SoA mirror (soa), host_idx, all_rank, slot_cell := cellnew[perm]
+// and, with rdst, the record tails (id, cell := new cell, dbg[1], spare)
+void launch_permute_fused(const int *perm, int n, const SoaMirror &src, const SoaMirror &dst,
+                          bool soa, const int *hid_src, int *hid_dst, const long long *ar_src,
+                          long long *ar_dst, const int *cellnew, int *slot_cell,
+                          const Particle *rsrc, Particle *rdst, cudaStream_t s);
+void launch_slot_cell_from_keys(int *slot_cell, const unsigned long long *keys, int n,
+                                cudaStream_t s);
 // FP64 DFMA throughput probe
 void launch_fp64_probe(double *out, int blocks, int iters, cudaStream_t s);
 
