@@ -1150,7 +1150,7 @@ struct sph_ctx {
   // (cell, all_rank) order from the last rebin, only the movers change cell and the stayers
   // keep their order, so the new order is a per-cell merge (kernels_layout.cu fixup_*), and
   // every per-slot array moves in one fused pass. Same result as the sort, byte for byte.
-  void rebin_fixup() {
+  void rebin_fixup(bool in_step) {
     const int N = (int)n;
     slot_cell_tmp.ensure(n); fx_moved.ensure(n + 1); fx_mpos.ensure(n + 1); fx_inlist.ensure(n);
     fx_perm.ensure(n); cellnew.ensure(n);
@@ -1168,7 +1168,9 @@ struct sph_ctx {
     F.scan_tmp = fx_scan.p; F.scan_bytes = sb;
     launch_rebin_fixup(F, stream);
     launched(6);
-    const bool soa_data = soa_valid || soa_ahead;
+    // the SoA mirror moves only when it is the truth (resident); an AoS-side copy is dropped
+    const bool soa_data = soa_ahead;
+    if (!soa_ahead) soa_valid = false;
     SoaMirror dst{};
     if (soa_data) {
       const size_t M = (size_t)n;
@@ -1188,7 +1190,7 @@ struct sph_ctx {
     // otherwise whole records, then p->cell
     launch_permute_fused(fx_perm.p, N, soa, dst, soa_data, host_idx.p, host_idx_tmp.p,
                          all_rank.p, all_rank_tmp.p, cellnew.p, slot_cell_tmp.p, aos.p,
-                         soa_ahead ? aos_tmp.p : nullptr, stream);
+                         soa_ahead ? aos_tmp.p : nullptr, in_step, stream);
     launched();
     if (!soa_ahead) {
       launch_permute<Particle>(aos_tmp.p, aos.p, fx_perm.p, N, stream);
@@ -1216,11 +1218,12 @@ struct sph_ctx {
     rebuild_worklist();
   }
 
-  void rebin() {
+  // in_step: called between drift and density by sph_step / sph_step_host
+  void rebin(bool in_step = false) {
     if (n == 0) return;
     need_rebin = false;
     if (fixup_ok && rebin_fixup_on) {
-      rebin_fixup();
+      rebin_fixup(in_step);
       return;
     }
     const bool soa_src = soa_ahead;
@@ -1520,7 +1523,7 @@ int sph_step(sph_ctx *ctx, const sph_params *par, double *kernel_ms) {
     CK(cudaEventRecord(e[1], ctx->stream));
     ctx->sweep(SPH_DRIFT, p, path);
     CK(cudaEventRecord(e[2], ctx->stream));
-    ctx->rebin();
+    ctx->rebin(true);
     CK(cudaEventRecord(e[3], ctx->stream));
     ctx->sweep(SPH_DENSITY, p, path);
     CK(cudaEventRecord(e[4], ctx->stream));
@@ -1553,7 +1556,7 @@ int sph_step_host(sph_ctx *ctx, void *const *recs, const sph_params *par, double
     CK(cudaEventRecord(e[2], ctx->stream));
     ctx->sweep(SPH_DRIFT, p, path);
     CK(cudaEventRecord(e[3], ctx->stream));
-    ctx->rebin();
+    ctx->rebin(true);
     CK(cudaEventRecord(e[4], ctx->stream));
     ctx->sweep(SPH_DENSITY, p, path);
     CK(cudaEventRecord(e[5], ctx->stream));

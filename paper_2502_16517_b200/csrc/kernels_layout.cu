@@ -574,14 +574,17 @@ __global__ void fixup_newslot_kernel(int *__restrict__ perm, const int *__restri
 // Every per-slot array in one pass: dst[k] = src[perm[k]] for the SoA mirror (when it holds
 // data), host_idx, all_rank, the slot's cell, and (TAILS) the record fields without a SoA
 // array (id, cell := the new cell, dbg[1], spare), i.e. build_grid's p->cell write
-// (grid.cpp:156) fused into the move.
+// (grid.cpp:156) fused into the move. step_dead: the rebin inside a full step (sph_step),
+// where density then force rewrite a, rho, u_dt, wcount, rho_dh, rot_v, div_v, v_sig of
+// every particle before any kernel reads them (kernels.cpp:194-202, :369-376), so those
+// eight arrays are not moved.
 template <bool SOA, bool TAILS>
 __global__ void permute_fused_kernel(const int *__restrict__ perm, int n, SoaMirror src,
                                      SoaMirror dst, const int *__restrict__ hid_src,
                                      int *__restrict__ hid_dst, const long long *__restrict__ ar_src,
                                      long long *__restrict__ ar_dst, const int *__restrict__ cellnew,
                                      int *__restrict__ slot_cell, const Particle *__restrict__ rsrc,
-                                     Particle *__restrict__ rdst) {
+                                     Particle *__restrict__ rdst, bool step_dead) {
   const int k = blockIdx.x * blockDim.x + threadIdx.x;
   if (k >= n) return;
   const int s = perm[k];
@@ -590,13 +593,16 @@ __global__ void permute_fused_kernel(const int *__restrict__ perm, int n, SoaMir
   hid_dst[k] = hid_src[s];
   ar_dst[k] = ar_src[s];
   if (SOA) {
-    dst.x[k] = src.x[s]; dst.v[k] = src.v[s]; dst.vp[k] = src.vp[s]; dst.a[k] = src.a[s];
-    dst.m[k] = src.m[s]; dst.rho[k] = src.rho[s]; dst.p[k] = src.p[s]; dst.u[k] = src.u[s];
-    dst.u_pred[k] = src.u_pred[s]; dst.u_dt[k] = src.u_dt[s]; dst.c[k] = src.c[s];
-    dst.h[k] = src.h[s]; dst.wcount[k] = src.wcount[s]; dst.rho_dh[k] = src.rho_dh[s];
-    dst.rot_v[k] = src.rot_v[s]; dst.div_v[k] = src.div_v[s]; dst.v_sig[k] = src.v_sig[s];
+    dst.x[k] = src.x[s]; dst.v[k] = src.v[s]; dst.vp[k] = src.vp[s];
+    dst.m[k] = src.m[s]; dst.p[k] = src.p[s]; dst.u[k] = src.u[s];
+    dst.u_pred[k] = src.u_pred[s]; dst.c[k] = src.c[s]; dst.h[k] = src.h[s];
     dst.h_dt[k] = src.h_dt[s]; dst.dt_next[k] = src.dt_next[s]; dst.dbg0[k] = src.dbg0[s];
     dst.frozen[k] = src.frozen[s]; dst.moved[k] = src.moved[s]; dst.flags[k] = src.flags[s];
+    if (!step_dead) { // fields the step's density / force write before anything reads them
+      dst.a[k] = src.a[s]; dst.rho[k] = src.rho[s]; dst.u_dt[k] = src.u_dt[s];
+      dst.wcount[k] = src.wcount[s]; dst.rho_dh[k] = src.rho_dh[s]; dst.rot_v[k] = src.rot_v[s];
+      dst.div_v[k] = src.div_v[s]; dst.v_sig[k] = src.v_sig[s];
+    }
   }
   if (TAILS) {
     const uint4 *a = reinterpret_cast<const uint4 *>(rsrc + s);
@@ -887,17 +893,17 @@ void launch_rebin_fixup(const FixupArgs &a, cudaStream_t s) {
 void launch_permute_fused(const int *perm, int n, const SoaMirror &src, const SoaMirror &dst,
                           bool soa, const int *hid_src, int *hid_dst, const long long *ar_src,
                           long long *ar_dst, const int *cellnew, int *slot_cell,
-                          const Particle *rsrc, Particle *rdst, cudaStream_t s) {
+                          const Particle *rsrc, Particle *rdst, bool step_dead, cudaStream_t s) {
   if (n <= 0) return;
   const int g = (n + 255) / 256;
   if (soa && rdst)
-    permute_fused_kernel<true, true><<<g, 256, 0, s>>>(perm, n, src, dst, hid_src, hid_dst, ar_src, ar_dst, cellnew, slot_cell, rsrc, rdst);
+    permute_fused_kernel<true, true><<<g, 256, 0, s>>>(perm, n, src, dst, hid_src, hid_dst, ar_src, ar_dst, cellnew, slot_cell, rsrc, rdst, step_dead);
   else if (soa)
-    permute_fused_kernel<true, false><<<g, 256, 0, s>>>(perm, n, src, dst, hid_src, hid_dst, ar_src, ar_dst, cellnew, slot_cell, rsrc, rdst);
+    permute_fused_kernel<true, false><<<g, 256, 0, s>>>(perm, n, src, dst, hid_src, hid_dst, ar_src, ar_dst, cellnew, slot_cell, rsrc, rdst, step_dead);
   else if (rdst)
-    permute_fused_kernel<false, true><<<g, 256, 0, s>>>(perm, n, src, dst, hid_src, hid_dst, ar_src, ar_dst, cellnew, slot_cell, rsrc, rdst);
+    permute_fused_kernel<false, true><<<g, 256, 0, s>>>(perm, n, src, dst, hid_src, hid_dst, ar_src, ar_dst, cellnew, slot_cell, rsrc, rdst, step_dead);
   else
-    permute_fused_kernel<false, false><<<g, 256, 0, s>>>(perm, n, src, dst, hid_src, hid_dst, ar_src, ar_dst, cellnew, slot_cell, rsrc, rdst);
+    permute_fused_kernel<false, false><<<g, 256, 0, s>>>(perm, n, src, dst, hid_src, hid_dst, ar_src, ar_dst, cellnew, slot_cell, rsrc, rdst, step_dead);
 }
 void launch_slot_cell_from_keys(int *slot_cell, const unsigned long long *keys, int n,
                                 cudaStream_t s) {

@@ -127,7 +127,7 @@ void launch_rebin_fixup(const FixupArgs &a, cudaStream_t s);
 void launch_permute_fused(const int *perm, int n, const SoaMirror &src, const SoaMirror &dst,
                           bool soa, const int *hid_src, int *hid_dst, const long long *ar_src,
                           long long *ar_dst, const int *cellnew, int *slot_cell,
-                          const Particle *rsrc, Particle *rdst, cudaStream_t s);
+                          const Particle *rsrc, Particle *rdst, bool step_dead, cudaStream_t s);
 void launch_slot_cell_from_keys(int *slot_cell, const unsigned long long *keys, int n,
                                 cudaStream_t s);
 // FP64 DFMA throughput probe
