@@ -200,6 +200,22 @@ int sph_dd_append(sph_ctx *ctx, const void *dev_recs, const int64_t *dev_ranks, 
 int sph_dd_export_rho(sph_ctx *ctx, const uint8_t *col_mask, double *dev_out, int64_t cap,
                       int64_t *count);
 int sph_dd_import_rho(sph_ctx *ctx, const uint8_t *col_mask, const double *dev_in, int64_t m);
+/* Halo records as the pair sweeps read them from an active particle that is not a local of
+ * an owned cell: x[2], v_pred[2], m, p, c (7 doubles = 56 B per particle, kernels.cpp:379-456
+ * ActiveView fields minus rho, which follows after density through sph_dd_export_rho) plus
+ * the all-rank. sph_dd_append_halo adds such particles (every other field zero); they must
+ * stay outside the owned cells and be dropped (sph_dd_remove) after the step. */
+int sph_dd_export_halo(sph_ctx *ctx, const uint8_t *col_mask, double *dev_out, int64_t *dev_ranks,
+                       int64_t cap, int64_t *count);
+int sph_dd_append_halo(sph_ctx *ctx, const double *dev_in, const int64_t *dev_ranks, int64_t m);
+/* The force sweep on the owned cells c with cell_mask[c] != 0 (HOST array of ncells bytes):
+ * a decomposed step runs the halo-independent interior while the halo rho is in flight. */
+int sph_sweep_cells(sph_ctx *ctx, int kernel, const sph_params *par, const uint8_t *cell_mask);
+/* Run the context's device work on `stream` (a cudaStream_t; NULL: the context's own), e.g.
+ * the caller's NCCL-ordered stream. */
+int sph_set_stream(sph_ctx *ctx, void *stream);
+/* Local particle count of every cell (ncells int64 values, HOST array). */
+int sph_cell_counts(sph_ctx *ctx, int64_t *out);
 /* Current particle count of the context. */
 int64_t sph_count(const sph_ctx *ctx);
 

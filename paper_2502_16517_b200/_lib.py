@@ -74,6 +74,11 @@ SIGNATURES = {
     "sph_dd_append": (C.c_int, [_vp, _vp, _vp, C.c_int64]),
     "sph_dd_export_rho": (C.c_int, [_vp, _vp, _vp, C.c_int64, C.POINTER(C.c_int64)]),
     "sph_dd_import_rho": (C.c_int, [_vp, _vp, _vp, C.c_int64]),
+    "sph_dd_export_halo": (C.c_int, [_vp, _vp, _vp, _vp, C.c_int64, C.POINTER(C.c_int64)]),
+    "sph_dd_append_halo": (C.c_int, [_vp, _vp, _vp, C.c_int64]),
+    "sph_sweep_cells": (C.c_int, [_vp, C.c_int, C.POINTER(SphParamsC), _vp]),
+    "sph_set_stream": (C.c_int, [_vp, _vp]),
+    "sph_cell_counts": (C.c_int, [_vp, _vp]),
 }
 
 _lib = None

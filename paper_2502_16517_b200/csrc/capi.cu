@@ -61,6 +61,20 @@ template <class T> struct DevBuf {
     p = nullptr;
     cap = 0;
   }
+  // capacity for `need` elements keeping the first `keep` (25 % headroom on growth)
+  void reserve_keep(size_t need, size_t keep, cudaStream_t st) {
+    if (need <= cap && p) return;
+    const size_t nc = std::max<size_t>(need + need / 4, 1);
+    T *q = nullptr;
+    CK(cudaMalloc(&q, nc * sizeof(T)));
+    if (p && keep) CK(cudaMemcpyAsync(q, p, std::min(keep, cap) * sizeof(T), cudaMemcpyDeviceToDevice, st));
+    if (p) {
+      CK(cudaStreamSynchronize(st));
+      CK(cudaFree(p));
+    }
+    p = q;
+    cap = nc;
+  }
 };
 
 struct PinnedBuf {
@@ -220,14 +234,15 @@ struct sph_ctx {
 
   DevBuf<int> cell_begin, cnt, pend_cnt, pend_cnt2, na_cell, ilist, pend_a, pend_b, host_idx, host_idx_tmp,
       cellnew, vals, vals_sorted, scalars;
-  DevBuf<long long> all_rank, all_rank_tmp, pairs_dev; // pairs_dev: {sum nl*na, particles}
+  DevBuf<long long> all_rank, all_rank_tmp, pairs_dev, pairs_dev2; // {sum nl*na, particles}
   DevBuf<unsigned long long> fail_dev; // density: particles that hit the 30-round limit
   DevBuf<unsigned long long> keys, keys_sorted;
   DevBuf<unsigned> cost_key, cost_key_sorted;
   DevBuf<unsigned char> owned;
   bool has_owned = false;
   DevBuf<int> cell_order, cell_order_in;
-  DevBuf<Item> items0, items_a, items_b, items_g;
+  DevBuf<Item> items0, items_a, items_b, items_c, items_d2, items_g;
+  DevBuf<int> cnt_sp, cnt_dn;
   DevBuf<int> hdep;
   DevBuf<double> hcur, wc;
   DevBuf<unsigned char> rounds, again;
@@ -245,7 +260,10 @@ struct sph_ctx {
   PinnedBuf h_stage, h_small;
   int n_items0 = 0;
   bool need_rebin = false; // particles were appended: cell lists stale until sph_rebin
-  DevBuf<unsigned char> dd_mask, dd_flag;
+  DevBuf<unsigned char> dd_mask, dd_flag, sub_mask;
+  DevBuf<int> sub_cnt;
+  DevBuf<Item> items_sub;
+  cudaStream_t own_stream = nullptr; // the stream sph_create made (sph_set_stream may replace `stream`)
   DevBuf<int> dd_sel, dd_cnt;
   DevBuf<int> mi_k, mi_off;
   DevBuf<char> mi_tmp;
@@ -284,7 +302,7 @@ struct sph_ctx {
       if (e) cudaEventDestroy(e);
     for (auto &e : rev)
       if (e) cudaEventDestroy(e);
-    if (stream) cudaStreamDestroy(stream);
+    if (own_stream) cudaStreamDestroy(own_stream);
     aos.release(); aos_tmp.release(); lin_recs.release(); fail_dev.release();
     f_x.release(); f_v.release(); f_vp.release(); f_a.release(); tmp2.release();
     f_m.release(); f_rho.release(); f_p.release(); f_u.release(); f_upred.release();
@@ -299,7 +317,8 @@ struct sph_ctx {
     cell_order.release(); cell_order_in.release(); items0.release(); items_a.release();
     items_b.release(); hcur.release(); wc.release(); rounds.release(); dense.release();
     cub_tmp.release(); h_stage.release(); h_small.release(); owned.release();
-    items_g.release(); hdep.release();
+    items_c.release(); items_d2.release(); cnt_sp.release(); cnt_dn.release(); pairs_dev2.release();
+    items_g.release(); hdep.release(); sub_mask.release(); sub_cnt.release(); items_sub.release();
     dd_mask.release(); dd_flag.release(); dd_sel.release(); dd_cnt.release();
     mi_k.release(); mi_off.release(); mi_tmp.release();
     jv_xy.release(); jv_vv.release(); jv_mg.release(); jv_pv.release(); jv_m.release(); jv_c.release();
@@ -336,6 +355,37 @@ struct sph_ctx {
                     f_udt.p, f_c.p, f_h.p, f_wc.p, f_rdh.p, f_rot.p, f_div.p, f_vsig.p,
                     f_hdt.p, f_dtn.p, f_dbg0.p, f_frozen.p, f_moved.p, f_flags.p};
     soa_alloc = true;
+  }
+
+  SoaMirror soa_at(int64_t off) const {
+    SoaMirror f = soa;
+    f.x += off; f.v += off; f.vp += off; f.a += off; f.m += off; f.rho += off; f.p += off;
+    f.u += off; f.u_pred += off; f.u_dt += off; f.c += off; f.h += off; f.wcount += off;
+    f.rho_dh += off; f.rot_v += off; f.div_v += off; f.v_sig += off; f.h_dt += off;
+    f.dt_next += off; f.dbg0 += off; f.frozen += off; f.moved += off; f.flags += off;
+    return f;
+  }
+
+  // Room for nn particles in every per-slot array that holds state (the first n kept).
+  void grow_state(int64_t nn) {
+    const size_t N = (size_t)nn, K = (size_t)n;
+    aos.reserve_keep(N, K, stream);
+    all_rank.reserve_keep(N, K, stream);
+    host_idx.reserve_keep(N, K, stream);
+    if (soa_alloc) {
+      f_x.reserve_keep(N, K, stream); f_v.reserve_keep(N, K, stream); f_vp.reserve_keep(N, K, stream);
+      f_a.reserve_keep(N, K, stream); f_m.reserve_keep(N, K, stream); f_rho.reserve_keep(N, K, stream);
+      f_p.reserve_keep(N, K, stream); f_u.reserve_keep(N, K, stream); f_upred.reserve_keep(N, K, stream);
+      f_udt.reserve_keep(N, K, stream); f_c.reserve_keep(N, K, stream); f_h.reserve_keep(N, K, stream);
+      f_wc.reserve_keep(N, K, stream); f_rdh.reserve_keep(N, K, stream); f_rot.reserve_keep(N, K, stream);
+      f_div.reserve_keep(N, K, stream); f_vsig.reserve_keep(N, K, stream); f_hdt.reserve_keep(N, K, stream);
+      f_dtn.reserve_keep(N, K, stream); f_dbg0.reserve_keep(N, K, stream);
+      f_frozen.reserve_keep(N, K, stream); f_moved.reserve_keep(N, K, stream);
+      f_flags.reserve_keep(N, K, stream);
+      soa = SoaMirror{f_x.p, f_v.p, f_vp.p, f_a.p, f_m.p, f_rho.p, f_p.p, f_u.p, f_upred.p,
+                      f_udt.p, f_c.p, f_h.p, f_wc.p, f_rdh.p, f_rot.p, f_div.p, f_vsig.p,
+                      f_hdt.p, f_dtn.p, f_dbg0.p, f_frozen.p, f_moved.p, f_flags.p};
+    }
   }
 
   void alloc_for(int64_t nn, int nc) {
@@ -490,11 +540,29 @@ struct sph_ctx {
     int *pend_out = pend_a.p;
     int *cnt_out = pend_cnt.p;
     Item *items_next = items_a.p;
-    for (int r = 0; r < 30 && nitems > 0; ++r) {
+    // rounds >= 1 (lean kernel, js1 > 1): j-slices pay while a cell's pending particles are
+    // sparse (their warps' boxes stay small); when most of a cell is pending, full warps are
+    // compact already and one lane per particle is faster (2^24: round 1 93.3 -> 91.0 ms; at
+    // 2^21, ~12 % pending, two lanes win: 4.9 -> 4.2 ms). The choice is made per cell from
+    // the cell's own pending share, so a cell's summation order (and its FAST result) does
+    // not depend on which other cells a context holds (k decomposed ranks == one rank).
+    const bool split = lean && js1 > 1;
+    const Item *items_d = nullptr; // the round's one-lane-per-particle items (dense cells)
+    int nitems_d = 0;
+    Item *items_next_d = items_c.p;
+    if (split) {
+      items_c.ensure((size_t)ncells + (size_t)n / kTI + 1);
+      items_d2.ensure((size_t)ncells + (size_t)n / kTI + 1);
+      items_next_d = items_c.p;
+      cnt_sp.ensure(ncells);
+      cnt_dn.ensure(ncells);
+      pairs_dev2.ensure(2);
+    }
+    for (int r = 0; r < 30 && (nitems > 0 || nitems_d > 0); ++r) {
       A.items = items;
       A.list = list;
       A.round = r;
-      A.jslices = r == 0 ? js0 : js_next;
+      A.jslices = r == 0 ? js0 : js1;
       if (meanw) {
         launch_density_exact(A, nitems, use_aos, true, stream);
         launched();
@@ -503,35 +571,47 @@ struct sph_ctx {
       if (r < 4) CK(cudaEventRecord(rev[2 * r], stream));
       if (exact) launch_density_exact(A, nitems, use_aos, false, stream);
       else launch_density_fast(A, nitems, use_aos, stream);
+      if (nitems_d > 0) { // same round, dense cells, one lane per particle
+        DenArgs D = A;
+        D.items = items_d;
+        D.jslices = 1;
+        launch_density_fast(D, nitems_d, use_aos, stream);
+        launched();
+      }
       if (r < 4) CK(cudaEventRecord(rev[2 * r + 1], stream));
       launch_compact_pending(pend_out, cnt_out, list, cnt_cur, again.p, cell_begin.p, ncells,
                              stream);
-      js_next = js1;
-      launch_make_items(items_next, scalars.p, pairs_dev.p, cnt_out, cell_begin.p, na_cell.p,
-                        cell_order.p, ncells, stream, kTI / js_next, items_scratch());
-      launched(3);
       pairs_total += pairs;
       updates += pending;
       max_round = r + 1;
-      CK(cudaMemcpyAsync(h_small.p, scalars.p, sizeof(int), cudaMemcpyDeviceToHost, stream));
-      CK(cudaMemcpyAsync((char *)h_small.p + 8, pairs_dev.p, 2 * sizeof(long long),
-                         cudaMemcpyDeviceToHost, stream));
-      CK(cudaStreamSynchronize(stream));
-      nitems = *(int *)h_small.p;
-      pairs = *(long long *)((char *)h_small.p + 8);
-      pending = *(long long *)((char *)h_small.p + 16);
-      // j-slices pay while the pending particles are sparse (their warps' boxes stay small);
-      // when most of a cell is pending (large n: dt fixed, h small), full warps are compact
-      // already and one lane per particle is faster (2^24: round 1 93.3 -> 91.0 ms; at 2^21,
-      // ~12 % pending, two lanes win: 4.9 -> 4.2 ms)
-      if (js1 > 1 && nitems > 0 && (double)pairs > den_dense_frac * (double)active_pairs) {
-        js_next = 1;
+      if (split) {
+        launch_split_pending(cnt_sp.p, cnt_dn.p, cnt_out, cnt.p, den_dense_frac, ncells, stream);
+        launch_make_items(items_next, scalars.p, pairs_dev.p, cnt_sp.p, cell_begin.p, na_cell.p,
+                          cell_order.p, ncells, stream, kTI / js1, items_scratch());
+        launch_make_items(items_next_d, scalars.p + 1, pairs_dev2.p, cnt_dn.p, cell_begin.p,
+                          na_cell.p, cell_order.p, ncells, stream, kTI, items_scratch());
+        launched(8);
+        CK(cudaMemcpyAsync(h_small.p, scalars.p, 2 * sizeof(int), cudaMemcpyDeviceToHost, stream));
+        CK(cudaMemcpyAsync((char *)h_small.p + 8, pairs_dev.p, 2 * sizeof(long long),
+                           cudaMemcpyDeviceToHost, stream));
+        CK(cudaMemcpyAsync((char *)h_small.p + 24, pairs_dev2.p, 2 * sizeof(long long),
+                           cudaMemcpyDeviceToHost, stream));
+        CK(cudaStreamSynchronize(stream));
+        nitems = ((int *)h_small.p)[0];
+        nitems_d = ((int *)h_small.p)[1];
+        pairs = *(long long *)((char *)h_small.p + 8) + *(long long *)((char *)h_small.p + 24);
+        pending = *(long long *)((char *)h_small.p + 16) + *(long long *)((char *)h_small.p + 32);
+      } else {
         launch_make_items(items_next, scalars.p, pairs_dev.p, cnt_out, cell_begin.p, na_cell.p,
-                          cell_order.p, ncells, stream, kTI, items_scratch());
-        launched();
+                          cell_order.p, ncells, stream, kTI / js1, items_scratch());
+        launched(3);
         CK(cudaMemcpyAsync(h_small.p, scalars.p, sizeof(int), cudaMemcpyDeviceToHost, stream));
+        CK(cudaMemcpyAsync((char *)h_small.p + 8, pairs_dev.p, 2 * sizeof(long long),
+                           cudaMemcpyDeviceToHost, stream));
         CK(cudaStreamSynchronize(stream));
         nitems = *(int *)h_small.p;
+        pairs = *(long long *)((char *)h_small.p + 8);
+        pending = *(long long *)((char *)h_small.p + 16);
       }
       if (r < 4) {
         float ms = 0;
@@ -540,9 +620,11 @@ struct sph_ctx {
       }
       // next round reads what this one produced
       items = items_next;
+      items_d = items_next_d;
       list = pend_out;
       cnt_cur = cnt_out;
       items_next = (items_next == items_a.p) ? items_b.p : items_a.p;
+      items_next_d = (items_next_d == items_c.p) ? items_d2.p : items_c.p;
       pend_out = (pend_out == pend_a.p) ? pend_b.p : pend_a.p;
       cnt_out = (cnt_out == pend_cnt.p) ? pend_cnt2.p : pend_cnt.p;
     }
@@ -558,10 +640,15 @@ struct sph_ctx {
     }
   }
 
-  void run_force(bool use_aos, bool exact, const Params &par) {
+  void run_force(bool use_aos, bool exact, const Params &par, const Item *items = nullptr,
+                 int nitems = -1) {
+    if (!items) {
+      items = items0.p;
+      nitems = n_items0;
+    }
     ForArgs A{};
     A.g = geom();
-    A.items = items0.p;
+    A.items = items;
     A.list = ilist.p;
     A.grav = par.grav;
     A.aos = aos.p;
@@ -573,14 +660,14 @@ struct sph_ctx {
       jv2_fblk.ensure(jv_blocks() * kF2Blk);
       F2Args B{};
       B.g = A.g;
-      B.items = items0.p;
+      B.items = items;
       B.list = ilist.p;
       B.grav = par.grav;
       B.aos = use_aos ? aos.p : nullptr;
       B.soa = soa;
       B.boxes = boxes.p;
       B.jv = F2View{jv2_fblk.p};
-      launch_force2(B, n_items0, (int)n, stream);
+      launch_force2(B, nitems, (int)n, stream);
       launched(3);
       stats.force_pairs = active_pairs;
       return;
@@ -600,8 +687,8 @@ struct sph_ctx {
       A.jv.pv = jv_pv.p;
       A.jv.c = jv_c.p;
     }
-    if (exact) launch_force_exact(A, n_items0, use_aos, stream);
-    else launch_force_fast(A, n_items0, use_aos, stream);
+    if (exact) launch_force_exact(A, nitems, use_aos, stream);
+    else launch_force_fast(A, nitems, use_aos, stream);
     launched();
     stats.force_pairs = active_pairs;
   }
@@ -783,10 +870,12 @@ struct sph_ctx {
   }
   int64_t dd_export(const uint8_t *col_mask, Particle *out, long long *ranks_out, int64_t cap) {
     if (n == 0) return 0;
-    make_aos_current();
     const int64_t m = dd_select(col_mask, false);
     if (m > cap) throw ArgError{"export buffer too small"};
-    launch_permute<Particle>(out, aos.p, dd_sel.p, (int)m, stream);
+    if (soa_ahead) // resident: assemble the selected records from the SoA mirror + tails
+      launch_export_soa(out, aos.p, soa, dd_sel.p, (int)m, stream);
+    else
+      launch_permute<Particle>(out, aos.p, dd_sel.p, (int)m, stream);
     if (ranks_out) launch_permute<long long>(ranks_out, all_rank.p, dd_sel.p, (int)m, stream);
     launched(2);
     CK(cudaStreamSynchronize(stream));
@@ -812,6 +901,23 @@ struct sph_ctx {
   void dd_append(const Particle *recs, const long long *ranks, int64_t m) {
     if (m <= 0) return;
     if (n + m >= (1LL << 31)) throw ArgError{"particle count out of range"};
+    if (soa_ahead || soa_valid) {
+      // resident: the records go to the AoS mirror and their fields straight into the SoA
+      // mirror at slots [n, n + m); the mirror state (SoA ahead or both valid) is kept
+      ensure_soa();
+      grow_state(n + m);
+      CK(cudaMemcpyAsync(aos.p + n, recs, sizeof(Particle) * m, cudaMemcpyDeviceToDevice, stream));
+      CK(cudaMemcpyAsync(all_rank.p + n, ranks, sizeof(long long) * m, cudaMemcpyDeviceToDevice, stream));
+      launch_gather(aos.p + n, soa_at(n), (int)m, kSoaFields, stream);
+      launched();
+      n += m;
+      fixup_ok = false;
+      alloc_for(n, ncells);
+      dd_reset_host_order();
+      need_rebin = true;
+      CK(cudaStreamSynchronize(stream));
+      return;
+    }
     make_aos_current();
     const int64_t nn = n + m;
     aos_tmp.ensure(nn);
@@ -863,8 +969,57 @@ struct sph_ctx {
     CK(cudaStreamSynchronize(stream));
   }
 
+  // Halo payload (x, v_pred, m, p, c: 7 doubles) + all-ranks of the selected particles.
+  int64_t dd_export_halo(const uint8_t *col_mask, double *out, long long *ranks_out, int64_t cap) {
+    if (n == 0) return 0;
+    make_soa_current();
+    const int64_t m = dd_select(col_mask, false);
+    if (m > cap) throw ArgError{"export buffer too small"};
+    launch_export_halo(out, soa, dd_sel.p, (int)m, stream);
+    if (ranks_out) launch_permute<long long>(ranks_out, all_rank.p, dd_sel.p, (int)m, stream);
+    launched(2);
+    CK(cudaStreamSynchronize(stream));
+    return m;
+  }
+  // Halo particles appended from their payload: SoA fields (the rest zero), zero record tails.
+  void dd_append_halo(const double *in, const long long *ranks, int64_t m) {
+    if (m <= 0) return;
+    if (n + m >= (1LL << 31)) throw ArgError{"particle count out of range"};
+    make_soa_current();
+    soa_ahead = true; // the appended particles exist in the SoA mirror only
+    grow_state(n + m);
+    CK(cudaMemsetAsync(aos.p + n, 0, sizeof(Particle) * m, stream));
+    CK(cudaMemcpyAsync(all_rank.p + n, ranks, sizeof(long long) * m, cudaMemcpyDeviceToDevice, stream));
+    launch_append_halo(soa_at(n), in, (int)m, stream);
+    launched();
+    n += m;
+    fixup_ok = false;
+    alloc_for(n, ncells);
+    dd_reset_host_order();
+    need_rebin = true;
+    CK(cudaStreamSynchronize(stream));
+  }
+
+  // Force on the owned cells with cell_mask[c] set (the halo-independent interior while the
+  // halo rho is in flight, then the rest): a work list of those cells only.
+  void force_cells(const Params &par, const uint8_t *cell_mask, int path) {
+    sub_mask.ensure(ncells);
+    sub_cnt.ensure(ncells);
+    items_sub.ensure((size_t)ncells + (size_t)n / kTI + 1);
+    CK(cudaMemcpyAsync(sub_mask.p, cell_mask, ncells, cudaMemcpyHostToDevice, stream));
+    launch_subset_counts(sub_cnt.p, cnt.p, sub_mask.p, ncells, stream);
+    launch_make_items(items_sub.p, scalars.p, pairs_dev.p, sub_cnt.p, cell_begin.p, na_cell.p,
+                      cell_order.p, ncells, stream, kTI, items_scratch());
+    launched(2);
+    CK(cudaMemcpyAsync(h_small.p, scalars.p, sizeof(int), cudaMemcpyDeviceToHost, stream));
+    CK(cudaStreamSynchronize(stream));
+    const int ni = *(int *)h_small.p;
+    sweep(SPH_FORCE, par, path, items_sub.p, ni);
+  }
+
   // One sweep on the device. Events: ev[0..3] bracket prologue / compute / epilogue.
-  void sweep(int kernel, const Params &par, int path) {
+  void sweep(int kernel, const Params &par, int path, const Item *f_items = nullptr,
+             int f_nitems = -1) {
     if (need_rebin && (kernel == SPH_DENSITY || kernel == SPH_FORCE))
       throw ArgError{"particles were appended: call sph_rebin before a pair sweep"};
     const int mode = mode_for(path);
@@ -883,7 +1038,7 @@ struct sph_ctx {
     CK(cudaEventRecord(ev[1], stream));
     const bool use_aos = mode == SPH_LAYOUT_AOS;
     if (kernel == SPH_DENSITY) run_density(use_aos, exact, par, false);
-    else if (kernel == SPH_FORCE) run_force(use_aos, exact, par);
+    else if (kernel == SPH_FORCE) run_force(use_aos, exact, par, f_items, f_nitems);
     else {
       launch_linear(kernel, use_aos, aos.p, soa, (int)n, par, stream);
       launched();
@@ -1344,6 +1499,7 @@ int sph_create(int device, sph_ctx **out) {
   if (const char *e = std::getenv("SPH_B200_DEN_DENSE")) ctx->den_dense_frac = std::atof(e);
   int r = guarded(ctx, [&] {
     CK(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
+    ctx->own_stream = ctx->stream;
     for (auto &e : ctx->ev) CK(cudaEventCreate(&e));
     for (auto &e : ctx->rev) CK(cudaEventCreate(&e));
     return SPH_OK;
@@ -1824,6 +1980,63 @@ int sph_dd_import_rho(sph_ctx *ctx, const uint8_t *col_mask, const double *dev_i
     dd_check(ctx, col_mask);
     if (m > 0 && !dev_in) throw ArgError{"null rho buffer"};
     ctx->dd_import_rho(col_mask, dev_in, m);
+    return SPH_OK;
+  });
+}
+
+int sph_dd_export_halo(sph_ctx *ctx, const uint8_t *col_mask, double *dev_out, int64_t *dev_ranks,
+                       int64_t cap, int64_t *count) {
+  return guarded(ctx, [&] {
+    dd_check(ctx, col_mask);
+    if (!dev_out && cap > 0) throw ArgError{"null halo buffer"};
+    const int64_t m = ctx->dd_export_halo(col_mask, dev_out, reinterpret_cast<long long *>(dev_ranks), cap);
+    if (count) *count = m;
+    return SPH_OK;
+  });
+}
+
+int sph_dd_append_halo(sph_ctx *ctx, const double *dev_in, const int64_t *dev_ranks, int64_t m) {
+  return guarded(ctx, [&] {
+    if (!ctx->bound) throw ArgError{"decomposition call before sph_bind"};
+    if (m < 0 || (m > 0 && (!dev_in || !dev_ranks))) throw ArgError{"bad halo append"};
+    ctx->dd_append_halo(dev_in, reinterpret_cast<const long long *>(dev_ranks), m);
+    ctx->stats.n = ctx->n;
+    return SPH_OK;
+  });
+}
+
+int sph_sweep_cells(sph_ctx *ctx, int kernel, const sph_params *par, const uint8_t *cell_mask) {
+  return guarded(ctx, [&] {
+    if (!ctx->bound) throw ArgError{"sph_sweep_cells before sph_bind"};
+    if (!par || !cell_mask) throw ArgError{"null argument"};
+    if (kernel != SPH_FORCE) throw ArgError{"sph_sweep_cells supports the force sweep only"};
+    if (ctx->need_rebin) throw ArgError{"particles were appended: call sph_rebin before a pair sweep"};
+    ctx->force_cells(to_params(par), cell_mask, SPH_PATH_AOS_BASELINE);
+    CK(cudaStreamSynchronize(ctx->stream));
+    float b = 0;
+    CK(cudaEventElapsedTime(&b, ctx->ev[1], ctx->ev[2]));
+    ctx->stats.last_force_ms = b;
+    return SPH_OK;
+  });
+}
+
+int sph_set_stream(sph_ctx *ctx, void *stream) {
+  return guarded(ctx, [&] {
+    CK(cudaStreamSynchronize(ctx->stream));
+    ctx->stream = stream ? static_cast<cudaStream_t>(stream) : ctx->own_stream;
+    return SPH_OK;
+  });
+}
+
+int sph_cell_counts(sph_ctx *ctx, int64_t *out) {
+  return guarded(ctx, [&] {
+    if (!ctx->bound) throw ArgError{"sph_cell_counts before sph_bind"};
+    if (!out) throw ArgError{"null output"};
+    std::vector<int> cb(ctx->ncells + 1);
+    CK(cudaMemcpyAsync(cb.data(), ctx->cell_begin.p, sizeof(int) * (ctx->ncells + 1),
+                       cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    for (int c = 0; c < ctx->ncells; ++c) out[c] = cb[c + 1] - cb[c];
     return SPH_OK;
   });
 }

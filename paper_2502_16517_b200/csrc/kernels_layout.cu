@@ -624,6 +624,97 @@ __global__ void slot_cell_from_keys_kernel(int *__restrict__ slot_cell,
   if (k < n) slot_cell[k] = (int)(keys[k] >> 40);
 }
 
+
+// ---- device-resident decomposition (sph_dd_*) ----
+// Records of the selected slots assembled from the SoA mirror (the truth in resident mode)
+// and the record fields without a SoA array, in selection order (migration export).
+__global__ void export_soa_kernel(uint4 *__restrict__ dense, const uint4 *__restrict__ aos,
+                                  SoaMirror f, const int *__restrict__ sel, long long total) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
+       i += (long long)gridDim.x * blockDim.x) {
+    const long long r = i / 17;
+    const int k = (int)(i - r * 17);
+    const int s = sel[r];
+    uint4 v;
+    auto two = [](double a, double b) {
+      return make_uint4(__double2loint(a), __double2hiint(a), __double2loint(b), __double2hiint(b));
+    };
+    switch (k) {
+    case 0: v = two(f.x[s].x, f.x[s].y); break;
+    case 1: v = two(f.v[s].x, f.v[s].y); break;
+    case 2: v = two(f.vp[s].x, f.vp[s].y); break;
+    case 3: v = two(f.a[s].x, f.a[s].y); break;
+    case 4: v = two(f.m[s], f.rho[s]); break;
+    case 5: v = two(f.p[s], f.u[s]); break;
+    case 6: v = two(f.u_pred[s], f.u_dt[s]); break;
+    case 7: v = two(f.c[s], f.h[s]); break;
+    case 8: v = two(f.wcount[s], f.rho_dh[s]); break;
+    case 9: v = two(f.rot_v[s], f.div_v[s]); break;
+    case 10: v = two(f.v_sig[s], f.h_dt[s]); break;
+    case 11: {
+      const double d = f.dt_next[s];
+      v = make_uint4(__double2loint(d), __double2hiint(d), (unsigned)f.frozen[s], (unsigned)f.moved[s]);
+      break;
+    }
+    case 13: {
+      const long long fl = f.flags[s];
+      const double d = f.dbg0[s];
+      v = make_uint4((unsigned)(fl & 0xffffffffLL), (unsigned)((unsigned long long)fl >> 32),
+                     __double2loint(d), __double2hiint(d));
+      break;
+    }
+    default: v = aos[(long long)s * 17 + k]; break; // id/cell, dbg[1], spare
+    }
+    dense[i] = v;
+  }
+}
+
+// Halo payload: the fields the pair sweeps read from an active particle that is not a local
+// of any owned cell, density's x, v_pred, m (kernels.cpp:379-392) plus force's p and c
+// (rho follows after density, sph_dd_export_rho): 7 doubles per particle.
+__global__ void export_halo_kernel(double *__restrict__ out, SoaMirror f,
+                                   const int *__restrict__ sel, int m) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= m) return;
+  const int s = sel[i];
+  double *o = out + 7LL * i;
+  o[0] = f.x[s].x; o[1] = f.x[s].y; o[2] = f.vp[s].x; o[3] = f.vp[s].y;
+  o[4] = f.m[s]; o[5] = f.p[s]; o[6] = f.c[s];
+}
+
+// Halo particles appended at slots [0, m) of `f` (offset mirror): the halo payload, every
+// other field zero (halo particles are never locals of an owned cell and are dropped after
+// the step).
+__global__ void append_halo_kernel(SoaMirror f, const double *__restrict__ in, int m) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= m) return;
+  const double *v = in + 7LL * i;
+  const double2 z = make_double2(0.0, 0.0);
+  f.x[i] = make_double2(v[0], v[1]); f.vp[i] = make_double2(v[2], v[3]);
+  f.m[i] = v[4]; f.p[i] = v[5]; f.c[i] = v[6];
+  f.v[i] = z; f.a[i] = z;
+  f.rho[i] = 0.0; f.u[i] = 0.0; f.u_pred[i] = 0.0; f.u_dt[i] = 0.0; f.h[i] = 0.0;
+  f.wcount[i] = 0.0; f.rho_dh[i] = 0.0; f.rot_v[i] = 0.0; f.div_v[i] = 0.0; f.v_sig[i] = 0.0;
+  f.h_dt[i] = 0.0; f.dt_next[i] = 0.0; f.dbg0[i] = 0.0;
+  f.frozen[i] = 0; f.moved[i] = 0; f.flags[i] = 0;
+}
+
+__global__ void split_pending_kernel(int *__restrict__ sp, int *__restrict__ dn,
+                                     const int *__restrict__ pend, const int *__restrict__ cnt,
+                                     double frac, int ncells) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= ncells) return;
+  const bool dense = (double)pend[c] > frac * (double)cnt[c];
+  sp[c] = dense ? 0 : pend[c];
+  dn[c] = dense ? pend[c] : 0;
+}
+
+__global__ void subset_counts_kernel(int *__restrict__ out, const int *__restrict__ cnt,
+                                     const unsigned char *__restrict__ mask, int ncells) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c < ncells) out[c] = mask[c] ? cnt[c] : 0;
+}
+
 __global__ void fp64_probe_kernel(double *out, int iters) {
   double a0 = threadIdx.x * 1e-9, a1 = a0 + 1e-9, a2 = a0 + 2e-9, a3 = a0 + 3e-9;
   double a4 = a0 + 4e-9, a5 = a0 + 5e-9, a6 = a0 + 6e-9, a7 = a0 + 7e-9;
@@ -908,6 +999,28 @@ void launch_permute_fused(const int *perm, int n, const SoaMirror &src, const So
 void launch_slot_cell_from_keys(int *slot_cell, const unsigned long long *keys, int n,
                                 cudaStream_t s) {
   if (n > 0) slot_cell_from_keys_kernel<<<(n + 255) / 256, 256, 0, s>>>(slot_cell, keys, n);
+}
+void launch_export_soa(Particle *dense, const Particle *aos, const SoaMirror &f, const int *sel,
+                       int m, cudaStream_t s) {
+  const long long total = 17LL * m;
+  if (m > 0)
+    export_soa_kernel<<<grid_for(total, 256), 256, 0, s>>>(reinterpret_cast<uint4 *>(dense),
+                                                            reinterpret_cast<const uint4 *>(aos),
+                                                            f, sel, total);
+}
+void launch_export_halo(double *out, const SoaMirror &f, const int *sel, int m, cudaStream_t s) {
+  if (m > 0) export_halo_kernel<<<(m + 255) / 256, 256, 0, s>>>(out, f, sel, m);
+}
+void launch_append_halo(const SoaMirror &f_at, const double *in, int m, cudaStream_t s) {
+  if (m > 0) append_halo_kernel<<<(m + 255) / 256, 256, 0, s>>>(f_at, in, m);
+}
+void launch_split_pending(int *sp, int *dn, const int *pend, const int *cnt, double frac,
+                          int ncells, cudaStream_t s) {
+  if (ncells > 0) split_pending_kernel<<<(ncells + 255) / 256, 256, 0, s>>>(sp, dn, pend, cnt, frac, ncells);
+}
+void launch_subset_counts(int *out, const int *cnt, const unsigned char *mask, int ncells,
+                          cudaStream_t s) {
+  if (ncells > 0) subset_counts_kernel<<<(ncells + 255) / 256, 256, 0, s>>>(out, cnt, mask, ncells);
 }
 void launch_fp64_probe(double *out, int blocks, int iters, cudaStream_t s) {
   fp64_probe_kernel<<<blocks, 256, 0, s>>>(out, iters);

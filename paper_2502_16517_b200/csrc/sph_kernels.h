@@ -130,6 +130,19 @@ void launch_permute_fused(const int *perm, int n, const SoaMirror &src, const So
                           const Particle *rsrc, Particle *rdst, bool step_dead, cudaStream_t s);
 void launch_slot_cell_from_keys(int *slot_cell, const unsigned long long *keys, int n,
                                 cudaStream_t s);
+// device-resident decomposition: records of the selected slots from the SoA mirror + record
+// tails (selection order); the 7-double halo payload (x, v_pred, m, p, c) out / in; the
+// per-cell counts of a cell subset
+void launch_export_soa(Particle *dense, const Particle *aos, const SoaMirror &f, const int *sel,
+                       int m, cudaStream_t s);
+void launch_export_halo(double *out, const SoaMirror &f, const int *sel, int m, cudaStream_t s);
+void launch_append_halo(const SoaMirror &f_at, const double *in, int m, cudaStream_t s);
+// density rounds >= 1: pending counts of the cells whose pending share is <= frac (sp, j-slice
+// items) and of the others (dn, one lane per particle)
+void launch_split_pending(int *sp, int *dn, const int *pend, const int *cnt, double frac,
+                          int ncells, cudaStream_t s);
+void launch_subset_counts(int *out, const int *cnt, const unsigned char *mask, int ncells,
+                          cudaStream_t s);
 // FP64 DFMA throughput probe
 void launch_fp64_probe(double *out, int blocks, int iters, cudaStream_t s);
 

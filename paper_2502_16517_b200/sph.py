@@ -305,6 +305,37 @@ class Context:
         _check(self.h, self.lib.sph_dd_import_rho(self.h, m.ctypes.data, in_ptr, count),
                "sph_dd_import_rho")
 
+    def dd_export_halo(self, col_mask: np.ndarray, out_ptr: int, ranks_ptr: int, cap: int) -> int:
+        """Halo payload (x, v_pred, m, p, c: 7 doubles per particle) + all-ranks of the
+        particles in the selected columns, in slot order."""
+        m = np.ascontiguousarray(col_mask, np.uint8)
+        out = C.c_int64()
+        _check(self.h, self.lib.sph_dd_export_halo(self.h, m.ctypes.data, out_ptr, ranks_ptr, cap,
+                                                   C.byref(out)), "sph_dd_export_halo")
+        return out.value
+
+    def dd_append_halo(self, in_ptr: int, ranks_ptr: int, count: int) -> None:
+        _check(self.h, self.lib.sph_dd_append_halo(self.h, in_ptr, ranks_ptr, count),
+               "sph_dd_append_halo")
+
+    def sweep_cells(self, k: KernelId, par: SphParams, cell_mask: np.ndarray) -> None:
+        """Force sweep on the owned cells with cell_mask[c] set."""
+        m = np.ascontiguousarray(cell_mask, np.uint8)
+        cp = _lib.SphParamsC(par.dt, par.gamma, par.cfl, par.grav, par.target_wcount)
+        _check(self.h, self.lib.sph_sweep_cells(self.h, int(k), C.byref(cp), m.ctypes.data),
+               "sph_sweep_cells")
+
+    def set_stream(self, stream_ptr: int | None) -> None:
+        """Run this context's device work on a caller's cudaStream_t (None: its own)."""
+        _check(self.h, self.lib.sph_set_stream(self.h, stream_ptr), "sph_set_stream")
+
+    def cell_counts(self) -> np.ndarray:
+        """Local particle count of every cell of the bound grid."""
+        st = self.stats()
+        out = np.zeros(max(st["ncells"], 1), np.int64)
+        _check(self.h, self.lib.sph_cell_counts(self.h, out.ctypes.data), "sph_cell_counts")
+        return out[: st["ncells"]]
+
     def read_records_all(self) -> np.ndarray:
         """Every record of the context in slot order (device-only contexts included)."""
         out = np.zeros(max(self.count(), 1), PARTICLE_DTYPE)

@@ -1,4 +1,4 @@
-"""Slab domain decomposition (paper_2502_16517_b200/decomp.py), world size 2 over gloo.
+"""Slab domain decomposition (paper_2502_16517_b200/decomp.py), world sizes 2-4 over gloo.
 
 The host-side logic (partition, migration, halo exchange, owned-cell sweeps) is checked
 on CPU with the oracle as the compute backend: k ranks must reproduce the single-rank
@@ -13,7 +13,8 @@ import numpy as np
 import pytest
 import torch.multiprocessing as mp
 
-from paper_2502_16517_b200.decomp import DistributedSim, Exchanger, SlabDecomposition, cell_of
+from paper_2502_16517_b200.decomp import (DistributedSim, Exchanger, SlabDecomposition,
+                                          balanced_bounds, cell_of, column_costs)
 
 N, PPC, SEED, DT, STEPS = 6000, 64, 4, 1e-2, 3
 
@@ -45,6 +46,14 @@ def _free_port():
     return p
 
 
+def decomposition(recs, nx, world, rank, balanced):
+    """Equal column counts, or (balanced) slabs of near-equal pair work from the IC."""
+    if not balanced:
+        return SlabDecomposition(nx, nx, world, rank)
+    counts = np.bincount(cell_of(recs, nx, nx), minlength=nx * nx)
+    return SlabDecomposition(nx, nx, world, rank, col_cost=column_costs(counts, nx, nx))
+
+
 def reference_run(orc, recs, par):
     r = recs.copy()
     nx = orc.grid_nx(len(r), PPC)
@@ -58,7 +67,7 @@ def reference_run(orc, recs, par):
     return r
 
 
-def _worker(rank, world, port, out_path, use_gpu):
+def _worker(rank, world, port, out_path, use_gpu, kind=0, balanced=False):
     import sys
     sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
     import torch.distributed as dist
@@ -69,11 +78,11 @@ def _worker(rank, world, port, out_path, use_gpu):
                             world_size=world)
     orc = Oracle()
     orc.threads = 2
-    recs, par = orc.make_particles(N, PPC, SEED)
+    recs, par = orc.make_particles(N, PPC, SEED, kind=kind)
     par = SphParams(dt=DT, gamma=par.gamma, cfl=par.cfl, grav=par.grav,
                     target_wcount=par.target_wcount)
     nx = orc.grid_nx(N, PPC)
-    d = SlabDecomposition(nx, nx, world, rank)
+    d = decomposition(recs, nx, world, rank, balanced)
     own, ranks = DistributedSim.split_global(recs, d)
     if use_gpu:
         from paper_2502_16517_b200.decomp import DeviceBackend
@@ -91,11 +100,11 @@ def _worker(rank, world, port, out_path, use_gpu):
     dist.destroy_process_group()
 
 
-def _run(world, use_gpu):
+def _run(world, use_gpu, kind=0, balanced=False):
     port = _free_port()
     with tempfile.TemporaryDirectory() as td:
         out = os.path.join(td, "out.npy")
-        mp.spawn(_worker, args=(world, port, out, use_gpu), nprocs=world, join=True)
+        mp.spawn(_worker, args=(world, port, out, use_gpu, kind, balanced), nprocs=world, join=True)
         return np.load(out)
 
 
@@ -124,17 +133,35 @@ def test_split_partitions_every_particle(orc):
     assert np.array_equal(allr, np.arange(3000))
 
 
-@pytest.mark.parametrize("world", [2, 3])
-def test_decomposed_steps_equal_single_rank(orc, world):
-    """world ranks (gloo, oracle compute) == the single-rank reference, byte for byte."""
+@pytest.mark.parametrize("world,kind,balanced", [(2, 0, False), (3, 0, False), (4, 0, False),
+                                                 (2, 1, False), (3, 1, True), (4, 0, True)])
+def test_decomposed_steps_equal_single_rank(orc, world, kind, balanced):
+    """world ranks (gloo, oracle compute; compact halo records: 40 B before density, 64 B
+    before force) == the single-rank reference, byte for byte: uniform and clustered
+    (variable ppc) boxes, equal-column and pair-work-balanced slabs."""
     from paper_2502_16517_b200 import SphParams
-    recs, par = orc.make_particles(N, PPC, SEED)
+    recs, par = orc.make_particles(N, PPC, SEED, kind=kind)
     par = SphParams(dt=DT, gamma=par.gamma, cfl=par.cfl, grav=par.grav,
                     target_wcount=par.target_wcount)
     ref = reference_run(orc, recs, par)
     assert np.count_nonzero(ref["cell"] != recs["cell"]) > 0  # particles changed cells
-    got = _run(world, use_gpu=False)
+    got = _run(world, use_gpu=False, kind=kind, balanced=balanced)
     assert got.tobytes() == ref.tobytes()
+
+
+def test_balanced_bounds_even_out_pair_work(orc):
+    """On a clustered box the pair-work-balanced slabs differ from equal columns and spread
+    the pair work more evenly; on equal costs they are the equal-column slabs."""
+    recs, _ = orc.make_particles(20000, 64, 3, kind=1)
+    nx = orc.grid_nx(20000, 64)
+    cost = column_costs(np.bincount(cell_of(recs, nx, nx), minlength=nx * nx), nx, nx)
+    for world in (2, 4):
+        eq = [(r * nx) // world for r in range(world + 1)]
+        bb = balanced_bounds(cost, world)
+        spread = lambda b: max(cost[b[r]:b[r + 1]].sum() for r in range(world)) / (cost.sum() / world)
+        assert spread(bb) <= spread(eq)
+        assert all(bb[r + 1] - bb[r] >= 2 for r in range(world))
+    assert balanced_bounds(np.ones(128), 8) == [16 * r for r in range(9)]
 
 
 @pytest.mark.gpu
@@ -149,7 +176,7 @@ def test_decomposed_steps_on_device_equal_single_rank(orc):
     assert got.tobytes() == ref.tobytes()
 
 
-def _dev_worker(rank, world, port, out_path, numerics_name):
+def _dev_worker(rank, world, port, out_path, numerics_name, kind=0, balanced=False):
     import sys
     sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
     import torch
@@ -162,11 +189,12 @@ def _dev_worker(rank, world, port, out_path, numerics_name):
                                 world_size=world)
     torch.cuda.set_device(0)
     ctx = Context(0, numerics=Numerics[numerics_name], layout=DeviceLayout.Resident)
-    par = ctx.make_particles_device(N, PPC, SEED)
+    par = ctx.make_particles_device(N, PPC, SEED, kind=kind)
     par.dt = DT
     import math
     nx = max(1, int(math.floor(1.0 / math.sqrt(PPC / N))))  # grid.cpp:23-26
-    d = SlabDecomposition(nx, nx, world, rank)
+    cost = column_costs(ctx.cell_counts(), nx, nx) if balanced else None
+    d = SlabDecomposition(nx, nx, world, rank, col_cost=cost)
     DeviceSlabSim.start(ctx, d)
     sim = DeviceSlabSim(ctx, d)
     for _ in range(STEPS):
@@ -181,11 +209,12 @@ def _dev_worker(rank, world, port, out_path, numerics_name):
     ctx.close()
 
 
-def _run_dev(world, numerics_name):
+def _run_dev(world, numerics_name, kind=0, balanced=False):
     port = _free_port()
     with tempfile.TemporaryDirectory() as td:
         out = os.path.join(td, "out.npy")
-        mp.spawn(_dev_worker, args=(world, port, out, numerics_name), nprocs=world, join=True)
+        mp.spawn(_dev_worker, args=(world, port, out, numerics_name, kind, balanced),
+                 nprocs=world, join=True)
         return np.load(out)
 
 
@@ -204,12 +233,15 @@ def test_device_resident_decomposition_exact_equals_reference(orc):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("world", [2, 3])
-def test_device_resident_decomposition_fast_equals_one_rank(world):
+@pytest.mark.parametrize("world,kind,balanced", [(2, 0, False), (3, 0, False), (4, 0, False),
+                                                 (2, 1, False), (4, 1, True)])
+def test_device_resident_decomposition_fast_equals_one_rank(world, kind, balanced):
     """FAST numerics: k device-resident ranks == one rank, byte for byte (each owned cell
-    sees the same active list in the same order, so even the reassociated FAST sums agree)."""
-    one = _run_dev(1, "Fast")
-    many = _run_dev(world, "Fast")
+    sees the same active list in the same order, so even the reassociated FAST sums agree;
+    the interior / boundary force split runs the same per-cell work), uniform and clustered
+    boxes, equal-column and pair-work-balanced slabs."""
+    one = _run_dev(1, "Fast", kind)
+    many = _run_dev(world, "Fast", kind, balanced)
     assert many.tobytes() == one.tobytes()
 
 
@@ -231,3 +263,13 @@ def test_device_slab_masks_are_consistent(nx, world):
         cols = np.nonzero(m["mine"])[0]
         for c in ((cols[0] - 1) % nx, (cols[-1] + 1) % nx):
             assert any(m["cols_of"][q][c] for q in m["peers"])
+    # the force split: interior + boundary = owned cells; no interior cell touches a halo column
+    for r in range(world):
+        d = SlabDecomposition(nx, nx, world, r)
+        inner, bnd = DeviceSlabSim.force_split(d)
+        own = d.owned_cells_mask().astype(np.uint8)
+        assert np.array_equal(inner + bnd, own) and not np.any(inner & bnd)
+        halo = set(d.halo_cols().tolist())
+        for c in np.nonzero(inner)[0]:
+            cx = c % nx
+            assert not ({(cx - 1) % nx, cx, (cx + 1) % nx} & halo)
