@@ -499,7 +499,8 @@ struct sph_ctx {
       if (force2 && A.g.use_shift) { // issue-lean density (any layout)
         jv2_x.ensure(n); jv2_y.ensure(n); jv2_m.ensure(n); jv2_vv.ensure(n);
         A.jv2 = D2View{jv2_x.p, jv2_y.p, jv2_m.p, jv2_vv.p};
-        launch_jview_density2(A.jv2, ilist.p, aos.p, soa, use_aos, (int)n, stream);
+        // the AoS arm stages its j's from the records (no j-view)
+        if (!use_aos) launch_jview_density2(A.jv2, ilist.p, aos.p, soa, use_aos, (int)n, stream);
       } else {
         jv_xy.ensure(n); jv_vv.ensure(n); jv_m.ensure(n);
         launch_jview_density(jv_xy.p, jv_vv.p, jv_m.p, ilist.p, aos.p, soa, use_aos, (int)n, stream);

@@ -496,6 +496,44 @@ __device__ __forceinline__ void force2_stage(F2Tile &T, const ActiveLayout &L, c
   cp_async_commit();
 }
 
+// AOS layout (the layout ablation's AoS arm): the chunk's j fields come straight from the
+// 272-B records, no j-view. Lane l copies j = 32 k + l of stencil cell nb: x, y, v_pred, c, m
+// and the raw (rho, p) into the tile's (P, V) slot; force2_convert_aos then turns
+// (m, rho, p) into the hoisted (grav m, m p / rho^2, m / rho) with stage_force's arithmetic,
+// so the tile holds exactly the j-view's values.
+__device__ __forceinline__ void force2_stage_aos(F2Tile &T, const ActiveLayout &L, const int *list,
+                                                 const Particle *aos, int nb, int k, int lane) {
+  const int q = k * kTJ + lane;
+  if (q < L.pre[nb + 1] - L.pre[nb]) {
+    const Particle *P = aos + list[L.base[nb] + q];
+    cp_async8(&T.x[lane], &P->x[0]);
+    cp_async8(&T.y[lane], &P->x[1]);
+    cp_async16(&T.vv[lane], P->v_pred);
+    cp_async8(&T.cm[lane].x, &P->c);
+    cp_async8(&T.cm[lane].y, &P->m);
+    cp_async8(&T.pv[lane].x, &P->rho);
+    cp_async8(&T.pv[lane].y, &P->p);
+  } else { // inert padding (jview_force2's dummies)
+    T.x[lane] = kDummyX;
+    T.y[lane] = kDummyX;
+    T.gm[lane] = 0.0;
+    T.vv[lane] = make_double2(0.0, 0.0);
+    T.pv[lane] = make_double2(0.0, 0.0);
+    T.cm[lane] = make_double2(0.0, 0.0);
+  }
+  cp_async_commit();
+}
+__device__ __forceinline__ void force2_convert_aos(F2Tile &T, const ActiveLayout &L, double grav,
+                                                   int nb, int k, int lane) {
+  if (k * kTJ + lane < L.pre[nb + 1] - L.pre[nb]) {
+    const double2 rp = T.pv[lane];
+    const double m = T.cm[lane].y;
+    const double4 d = FastPolicy::stage_force(m, rp.x, rp.y, grav); // (m, gm, P, V)
+    T.gm[lane] = d.y;
+    T.pv[lane] = make_double2(d.z, d.w);
+  }
+}
+
 template <int MINB, bool AOS>
 __global__ void __launch_bounds__(kF2W * 32, MINB) force2_kernel(F2Args A) {
   __shared__ F2Tile tiles[kF2W][2];
@@ -559,13 +597,21 @@ __global__ void __launch_bounds__(kF2W * 32, MINB) force2_kernel(F2Args A) {
       const bool has_next = todo != 0u;
       // one warp barrier per chunk: after it every lane's copies of this chunk are visible
       // and every lane is done with the previous chunk, whose buffer the next staging reuses
-      if (!staged) force2_stage(tiles[w][buf], L, A.jv, cnb, ck, lane);
+      if (!staged) {
+        if constexpr (AOS) force2_stage_aos(tiles[w][buf], L, A.list, A.aos, cnb, ck, lane);
+        else force2_stage(tiles[w][buf], L, A.jv, cnb, ck, lane);
+      }
       cp_async_wait<0>();
       __syncwarp();
+      if constexpr (AOS) {
+        force2_convert_aos(tiles[w][buf], L, A.grav, cnb, ck, lane);
+        __syncwarp();
+      }
       if (has_next) {
         const int bn = __ffs(todo) - 1;
         const int nnb = __shfl_sync(0xffffffffu, nb, bn), nk = __shfl_sync(0xffffffffu, kk, bn);
-        force2_stage(tiles[w][buf ^ 1], L, A.jv, nnb, nk, lane);
+        if constexpr (AOS) force2_stage_aos(tiles[w][buf ^ 1], L, A.list, A.aos, nnb, nk, lane);
+        else force2_stage(tiles[w][buf ^ 1], L, A.jv, nnb, nk, lane);
       }
       staged = has_next;
       const F2Tile &T = tiles[w][buf];
@@ -698,6 +744,25 @@ __device__ __forceinline__ void density2_stage(D2Tile &T, const ActiveLayout &L,
   cp_async_commit();
 }
 
+// AOS layout: the chunk's j fields (x, y, m, v_pred) straight from the 272-B records.
+__device__ __forceinline__ void density2_stage_aos(D2Tile &T, const ActiveLayout &L, const int *jlist,
+                                                   const Particle *aos, int nb, int k, int lane) {
+  const int q = k * kTJ + lane;
+  if (q < L.pre[nb + 1] - L.pre[nb]) {
+    const Particle *P = aos + jlist[L.base[nb] + q];
+    cp_async8(&T.x[lane], &P->x[0]);
+    cp_async8(&T.y[lane], &P->x[1]);
+    cp_async8(&T.m[lane], &P->m);
+    cp_async16(&T.vv[lane], P->v_pred);
+  } else {
+    T.x[lane] = kDummyX;
+    T.y[lane] = kDummyX;
+    T.m[lane] = 0.0;
+    T.vv[lane] = make_double2(0.0, 0.0);
+  }
+  cp_async_commit();
+}
+
 // density_pair (kernels.cpp:97-119) for one in-support pair, on FastPolicy's scaled sums
 // (the piece comes from r2 against per-i thresholds (0.5h)^2, (1.5h)^2 on the high words,
 // so the coefficient loads issue before the rsqrt chain; a pair within 2^-20 of a knot may
@@ -789,13 +854,17 @@ __global__ void __launch_bounds__(kD2W * 32, MINB) density2_kernel(DenArgs A) {
       todo &= todo - 1;
       const int cnb = __shfl_sync(0xffffffffu, nb, b), ck = __shfl_sync(0xffffffffu, kk, b);
       const bool has_next = todo != 0u;
-      if (!staged) density2_stage(tiles[w][buf], L, A.jv2, cnb, ck, lane);
+      if (!staged) {
+        if constexpr (AOS) density2_stage_aos(tiles[w][buf], L, A.jlist, A.aos, cnb, ck, lane);
+        else density2_stage(tiles[w][buf], L, A.jv2, cnb, ck, lane);
+      }
       cp_async_wait<0>();
       __syncwarp();
       if (has_next) {
         const int bn = __ffs(todo) - 1;
         const int nnb = __shfl_sync(0xffffffffu, nb, bn), nk = __shfl_sync(0xffffffffu, kk, bn);
-        density2_stage(tiles[w][buf ^ 1], L, A.jv2, nnb, nk, lane);
+        if constexpr (AOS) density2_stage_aos(tiles[w][buf ^ 1], L, A.jlist, A.aos, nnb, nk, lane);
+        else density2_stage(tiles[w][buf ^ 1], L, A.jv2, nnb, nk, lane);
       }
       staged = has_next;
       // per-j culling: a j farther than the warp's reach from the warp box can be in no
@@ -967,13 +1036,11 @@ __global__ void jview_force2_kernel(double *blk, const int *ilist, const int *ce
 
 void launch_force2(const F2Args &a, int n_items, int n, cudaStream_t s) {
   const bool aos = a.aos != nullptr;
-  if (n > 0 && a.g.ncells > 0) {
-    double *blk = const_cast<double *>(a.jv.blk);
-    if (aos)
-      jview_force2_kernel<true><<<a.g.ncells, 128, 0, s>>>(blk, a.list, a.g.cell_begin, a.aos, a.soa, a.grav);
-    else
-      jview_force2_kernel<false><<<a.g.ncells, 128, 0, s>>>(blk, a.list, a.g.cell_begin, a.aos, a.soa, a.grav);
-  }
+  // the SoA layouts read the per-sweep chunk-major j-view; the AoS arm stages j's from the
+  // records themselves (force2_stage_aos)
+  if (n > 0 && a.g.ncells > 0 && !aos)
+    jview_force2_kernel<false><<<a.g.ncells, 128, 0, s>>>(const_cast<double *>(a.jv.blk), a.list,
+                                                          a.g.cell_begin, a.aos, a.soa, a.grav);
   if (n_items <= 0) return;
   F2Args b = a;
   b.n_items = n_items;

@@ -297,3 +297,33 @@ def test_rebin_fixup_equals_sort(monkeypatch, layout, kind):
             moved.append(np.count_nonzero(np.sort(recs["cell"]) != np.sort(cell0)))
     assert moved[0] > 0, "test must exercise particles changing cells"
     assert outs[0] == outs[1]
+
+
+@pytest.mark.parametrize("kind", [0, 1])
+def test_aos_arm_stages_records_like_the_jview(orc, kind):
+    """The layout ablation's AoS arm reads every j field straight from the 272-B records
+    (no j-view; force's grav m, m p / rho^2, m / rho formed in the tile with the j-view's
+    arithmetic), so FAST density and force in the AoS layout equal the resident-SoA layout
+    byte for byte, and stay within the FAST tolerance of the oracle."""
+    n, ppc, seed = 30000, 128, 6
+    recs0, par = orc.make_particles(n, ppc, seed, kind=kind)
+    outs = []
+    for layout in (DeviceLayout.Aos, DeviceLayout.Resident):
+        recs = recs0.copy()
+        store = pkg.ParticleStore(recs, np.arange(n, dtype=np.int64), pkg.Layout.Continuous)
+        grid = pkg.build_grid(store, pkg.InitConfig(n=n, ppc=ppc))
+        ctx = pkg.Context(0, numerics=Numerics.Fast, layout=layout)
+        ctx.bind(grid)
+        with ctx:
+            ctx.run_sweep(KernelId.Density, par)
+            ctx.run_sweep(KernelId.Force, par)
+        outs.append(store.recs.copy())
+    assert outs[0].tobytes() == outs[1].tobytes()
+    ref = recs0.copy()
+    nx = orc.grid_nx(n, ppc)
+    cb, li = orc.build_grid(ref, nx)
+    for k in (KernelId.Density, KernelId.Force):
+        orc.sweep(int(k), ref, nx, nx, 1.0 / nx, cb, li, par)
+    sel = np.arange(n)
+    for f in DEN_FIELDS + FOR_FIELDS:
+        assert within(outs[0], ref, sel, f).mean() > 0.999, f
