@@ -54,9 +54,10 @@ def flops_per_pair(f_in, f15, f05):
     return 13 + 38 * f_in + 11 * f15 + 11 * f05, 22 + 45 * f_in + 5 * f15 + 5 * f05
 
 
-# algorithmic bytes per particle of the streaming kernels (descriptor bytes in + out,
-# kernels.cpp:808-859): drift 52+28, kick1 48+32, kick2 112+80
-LINEAR_BYTES = {"kick1": 80, "drift": 80, "kick2": 192}
+# bytes per particle the resident-SoA streaming kernels move: their view descriptors'
+# fields in + out (kernels.cpp:808-859), drift 52+28, kick1 48+32, kick2 104+80 (the SoA
+# mirror holds dbg[0] only, so kick2 reads 8 B less than its 112-B descriptor)
+LINEAR_BYTES = {"kick1": 80, "drift": 80, "kick2": 184}
 
 
 def load_peaks():
@@ -482,8 +483,12 @@ def _finish(out, ctx, store, grid, par, args, rank, world, ph, names, den_eval, 
         hbm = peaks.get("hbm_gbs", 6650.0)
         out["roofline_linear"] = {
             k: {"achieved_gbs": LINEAR_BYTES[k] * args.n / (ph[names.index(k)] * 1e-3) / 1e9,
+                "bytes_per_particle": LINEAR_BYTES[k],
                 "peak_gbs": hbm, "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({src})",
-                "frac": LINEAR_BYTES[k] * args.n / (ph[names.index(k)] * 1e-3) / 1e9 / hbm}
+                "frac": LINEAR_BYTES[k] * args.n / (ph[names.index(k)] * 1e-3) / 1e9 / hbm,
+                "note": "effective: bytes the kernel's fields occupy / kernel time; the peak "
+                        "is a copy (half reads, half writes), which a read-heavy kernel can "
+                        "exceed slightly"}
             for k in LINEAR_BYTES}
         out["pair_fractions"] = {"f_in": fin, "f_lt_1.5": f15, "f_lt_0.5": f05}
         if world == 1 and args.cpu_baseline:

@@ -1900,13 +1900,17 @@ int sph_fp64_peak(sph_ctx *ctx, double *tflops) {
     out.ensure(1);
     const int blocks = sms * 8, iters = 4096;
     launch_fp64_probe(out.p, blocks, 64, ctx->stream); // warm-up
-    CK(cudaEventRecord(ctx->ev[0], ctx->stream));
-    launch_fp64_probe(out.p, blocks, iters, ctx->stream);
-    CK(cudaEventRecord(ctx->ev[1], ctx->stream));
-    CK(cudaStreamSynchronize(ctx->stream));
-    ctx->launched(2);
     float ms = 0;
-    CK(cudaEventElapsedTime(&ms, ctx->ev[0], ctx->ev[1]));
+    for (int t = 0; t < 3; ++t) { // best of three (a peak, not an average)
+      CK(cudaEventRecord(ctx->ev[0], ctx->stream));
+      launch_fp64_probe(out.p, blocks, iters, ctx->stream);
+      CK(cudaEventRecord(ctx->ev[1], ctx->stream));
+      CK(cudaStreamSynchronize(ctx->stream));
+      float m = 0;
+      CK(cudaEventElapsedTime(&m, ctx->ev[0], ctx->ev[1]));
+      if (t == 0 || m < ms) ms = m;
+    }
+    ctx->launched(4);
     out.release();
     const double flops = 2.0 * 64.0 * 256.0 * (double)blocks * (double)iters;
     if (tflops) *tflops = flops / (ms * 1e-3) / 1e12;
