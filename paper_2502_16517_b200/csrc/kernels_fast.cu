@@ -373,6 +373,17 @@ __constant__ double2 kSplE[9] = {
     {1.5, -1.0}, {-4.0, 3.0}, {3.0, 1.0},  // q in [0.5, 1.5): -4s^3+3s^2+3s+1,    s = 1.5 - q
     {0.0, -1.0}, {6.0, 0.0}, {-7.5, 0.0},  // q in [0, 0.5):   6s^3 - 7.5s,        s = -q
 };
+#ifndef SPH_F2_QH
+#define SPH_F2_QH 1
+#endif
+
+// the same pieces as polynomials in q (SPH_F2_QH): E = ((a3 q + a2) q + a1) q + a0, rows of
+// two double2 {a3, a2}, {a1, a0}; saves the s = c_off - q DFMA, which reads three registers
+__constant__ double2 kSplQ[6] = {
+    {-1.0, 7.5}, {-18.75, 15.625}, // (2.5 - q)^3
+    {4.0, -15.0}, {15.0, -1.25},   // -4 s^3 + 3 s^2 + 3 s + 1, s = 1.5 - q
+    {-6.0, 0.0}, {7.5, 0.0},       // 6 s^3 - 7.5 s, s = -q
+};
 
 __device__ __forceinline__ void cp_async8(void *smem, const void *gmem) {
   const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
@@ -438,6 +449,16 @@ __device__ __forceinline__ double force2_sph(const F2I &I, const F2Tile &T, int 
                                              double dy, double r2, double k0375, double &udt,
                                              double &hdt, double &vsig, unsigned hiH2m1) {
   const int hr = __double2hiint(r2);
+#if SPH_F2_QH
+  int row = hr < I.hiQ15 ? 2 : 0;
+  if (hr < I.hiQ05) row = 4;
+  const double2 t1 = T.spl[row], t2 = T.spl[row + 1];
+  const double y0 = rsqrt_seed(r2);
+  const double e = fma(-r2, y0 * y0, 1.0);
+  const double rinv = fma(y0, e * fma(e, k0375, 0.5), y0);
+  const double q = (r2 * rinv) * I.inv_hi;
+  const double E = fma(fma(fma(t1.x, q, t1.y), q, t2.x), q, t2.y);
+#else
   int row = hr < I.hiQ15 ? 3 : 0;
   if (hr < I.hiQ05) row = 6;
   const double c_off = T.spl[row].x;
@@ -447,14 +468,16 @@ __device__ __forceinline__ double force2_sph(const F2I &I, const F2Tile &T, int 
   const double rinv = fma(y0, e * fma(e, k0375, 0.5), y0);
   const double s = fma(-(r2 * rinv), I.inv_hi, c_off);
   const double E = fma(fma(fma(t1.x, s, t1.y), s, t2.x), s, t2.y);
+#endif
   const double g = E * rinv;
   const double2 vj = T.vv[j];
   const double dvx = I.vx - vj.x, dvy = I.vy - vj.y;
   const double dvdr = fma(dvx, dx, dvy * dy);
   const double gd = g * dvdr;
   const double2 cm = T.cm[j], pv = T.pv[j];
-  udt = fma(cm.y, gd, udt);
-  hdt = fma(pv.y, gd, hdt);
+  // gd in the same operand slot of both updates (reuse cache)
+  udt = fma(gd, cm.y, udt);
+  hdt = fma(gd, pv.y, hdt);
   const double mu = (__double2hiint(dvdr) < 0 ? dvdr : 0.0) * rinv;
   const double vs = fma(mu, I.mb3, cm.x);
   if (__double_as_longlong(vs) > __double_as_longlong(vsig)) vsig = vs;
@@ -543,7 +566,11 @@ __global__ void __launch_bounds__(kF2W * 32, MINB) force2_kernel(F2Args A) {
   const int w = kF2W == 1 ? 0 : warp_in_cta(), lane = lane_id();
   const int item_idx = blockIdx.x * kF2W + w;
   if (item_idx >= A.n_items) return;
+#if SPH_F2_QH
+  if (lane < 6) tiles[w][0].spl[lane] = tiles[w][1].spl[lane] = kSplQ[lane];
+#else
   if (lane < 9) tiles[w][0].spl[lane] = tiles[w][1].spl[lane] = kSplE[lane];
+#endif
   if (lane == 0) tiles[w][0].edge = tiles[w][1].edge = 0;
   ActiveLayout &L = lay[w];
   const Item it = A.items[item_idx];
@@ -567,7 +594,11 @@ __global__ void __launch_bounds__(kF2W * 32, MINB) force2_kernel(F2Args A) {
     K = F.K;
     hiH2m1 = F.hiH2m1;
   }
-  double ax = 0.0, ay = 0.0, udt = 0.0, hdt = 0.0, vsig = -1.0;
+  // axn, ayn accumulate -a: fma(f, dx, axn) == -fma(-f, dx, ax) exactly (round to nearest is
+  // sign-symmetric), and with f un-negated in the same operand slot of the x and y updates
+  // ptxas serves the second read from the operand reuse cache (a DFMA reading three distinct
+  // 64-bit registers takes 3 FP64-pipe cycles instead of 2, tools/operand_probe.cu)
+  double axn = 0.0, ayn = 0.0, udt = 0.0, hdt = 0.0, vsig = -1.0;
   const float ixlo = warp_min((float)xi.x), ixhi = warp_max((float)xi.x);
   const float iylo = warp_min((float)xi.y), iyhi = warp_max((float)xi.y);
   const float reach = warp_max((float)(2.5 * hi)) * (1.0f + 1e-5f) + 1e-6f;
@@ -640,12 +671,12 @@ __global__ void __launch_bounds__(kF2W * 32, MINB) force2_kernel(F2Args A) {
           // registers inside it); same j order
           if (support_cand(r20, hiH2m1))
             f0 = fma(K, force2_sph(I, T, j, dx0, dy0, r20, k0375, udt, hdt, vsig, hiH2m1), f0);
-          ax = fma(-f0, dx0, ax);
-          ay = fma(-f0, dy0, ay);
+          axn = fma(f0, dx0, axn);
+          ayn = fma(f0, dy0, ayn);
           if (support_cand(r21, hiH2m1))
             f1 = fma(K, force2_sph(I, T, j + 1, dx1, dy1, r21, k0375, udt, hdt, vsig, hiH2m1), f1);
-          ax = fma(-f1, dx1, ax);
-          ay = fma(-f1, dy1, ay);
+          axn = fma(f1, dx1, axn);
+          ayn = fma(f1, dy1, ayn);
         }
         __syncwarp();
         if (T.edge) { // warp-uniform after the barrier; rare
@@ -676,8 +707,8 @@ __global__ void __launch_bounds__(kF2W * 32, MINB) force2_kernel(F2Args A) {
             const double e = fma(-s, t, 1.0);
             const double c = gm[u] * (t * y0);
             const double f = fma(c, e * fma(e, k1875, 1.5), c);
-            ax = fma(-f, dx[u], ax);
-            ay = fma(-f, dy[u], ay);
+            axn = fma(f, dx[u], axn);
+            ayn = fma(f, dy[u], ayn);
           }
         }
       }
@@ -689,7 +720,7 @@ __global__ void __launch_bounds__(kF2W * 32, MINB) force2_kernel(F2Args A) {
   const FastPolicy::FI F =
       FastPolicy::for_i(xi, src.vp(slot), hi, src.pr(slot), src.rho(slot), src.rho_dh(slot),
                         src.c(slot), src.div_v(slot), src.rot_v(slot), A.grav, nullptr);
-  FastPolicy::FA s{ax, ay, udt, vsig, hdt, src.h_dt(slot)};
+  FastPolicy::FA s{-axn, -ayn, udt, vsig, hdt, src.h_dt(slot)};
   double o[5];
   FastPolicy::for_publish(F, s, o);
   if constexpr (AOS) {
@@ -719,11 +750,26 @@ struct __align__(16) D2Tile {
 // E = P'(s) / 4, evaluated by the derivative Horner recursion alongside P: four table loads
 // instead of six, the same seven DFMA. Sums over m E carry the factor 4, removed at publish.
 // Rows are 4 entries apart; s = c_off - q on every piece.
+#ifndef SPH_D2_QH
+#define SPH_D2_QH 1
+#endif
+
+#if SPH_D2_QH
+// P as polynomials in q (SPH_D2_QH), rows {p4, p3}, {p2, p1}, {-, p0}: the same pieces,
+// (2.5-q)^4, (2.5-q)^4 - 5 (1.5-q)^4, ... + 10 (0.5-q)^4, expanded (exact binary
+// coefficients); dP/dq = -4 E, so the sums over m dP/dq carry the factor -4
+__constant__ double2 kSplPE[12] = {
+    {1.0, -10.0}, {37.5, -62.5}, {0.0, 39.0625}, {0.0, 0.0},
+    {-4.0, 20.0}, {-30.0, 5.0}, {0.0, 13.75}, {0.0, 0.0},
+    {6.0, 0.0}, {-15.0, 0.0}, {0.0, 14.375}, {0.0, 0.0},
+};
+#else
 __constant__ double2 kSplPE[12] = {
     {1.0, 0.0}, {0.0, 0.0}, {2.5, 0.0}, {0.0, 0.0},       // s^4,                     s = 2.5 - q
     {-4.0, 4.0}, {6.0, 4.0}, {1.5, 1.0}, {0.0, 0.0},      // -4s^4+4s^3+6s^2+4s+1,    s = 1.5 - q
     {6.0, 0.0}, {-15.0, 0.0}, {0.0, 14.375}, {0.0, 0.0},  // 6s^4-15s^2+14.375,       s = -q
 };
+#endif
 
 __device__ __forceinline__ void density2_stage(D2Tile &T, const ActiveLayout &L, const D2View &jv,
                                                int nb, int k, int lane) {
@@ -778,7 +824,11 @@ __device__ __forceinline__ void density2_pair(const FastPolicy::DI &I, int hiQ05
   const double e = fma(-r2, y0 * y0, 1.0);
   const double rinv = fma(y0, e * fma(e, k0375, 0.5), y0);
   const double r = r2 * rinv;
+#if SPH_D2_QH
+  const double sv = r * I.inv_h; // q
+#else
   const double sv = fma(-r, I.inv_h, t3.x); // c_off - q
+#endif
   const double b3 = fma(t1.x, sv, t1.y), b2 = fma(b3, sv, t2.x), b1 = fma(b2, sv, t2.y);
   const double P = fma(b1, sv, t3.y);
   const double D = fma(fma(fma(t1.x, sv, b3), sv, b2), sv, b1); // P'(s) = 4 E
@@ -951,9 +1001,14 @@ __global__ void __launch_bounds__(kD2W * 32, MINB) density2_kernel(DenArgs A) {
     }
   }
   if (!live || qs != 0) return;
-  s.qe *= 0.25 * I.inv_h; // accumulated as sum r (4 m E): to sum q m E
-  s.div *= 0.25;
-  s.rot *= 0.25;
+#if SPH_D2_QH
+  constexpr double kDs = -0.25; // accumulated with dP/dq = -4 E
+#else
+  constexpr double kDs = 0.25; // accumulated with dP/ds = 4 E
+#endif
+  s.qe *= kDs * I.inv_h; // accumulated as sum r (4 m E): to sum q m E
+  s.div *= kDs;
+  s.rot *= kDs;
   double hn = h;
   const int st = FastPolicy::den_step(s, hn, A.target, A.h_max, A.round);
   A.again[it.start + iw] = (unsigned char)(st == 0);
