@@ -236,6 +236,7 @@ struct sph_ctx {
       cellnew, vals, vals_sorted, scalars;
   DevBuf<long long> all_rank, all_rank_tmp, pairs_dev, pairs_dev2; // {sum nl*na, particles}
   DevBuf<unsigned long long> fail_dev; // density: particles that hit the 30-round limit
+  DevBuf<int> item_ctr;                 // density: persistent-round item counters
   DevBuf<unsigned long long> keys, keys_sorted;
   DevBuf<unsigned> cost_key, cost_key_sorted;
   DevBuf<unsigned char> owned;
@@ -255,6 +256,7 @@ struct sph_ctx {
   int force2 = 1; // FAST force on the resident SoA: issue-lean kernel (env SPH_B200_FORCE2=0: old)
   int den_js0 = 1, den_js1 = 2; // lean density: lanes per particle in round 0 / rounds >= 1
   double den_dense_frac = 0.35;  // rounds >= 1 use one lane per particle above this pending share
+  bool dev_rounds = true; // density rounds >= 1 queued with device-side item counts (env SPH_B200_DEV_ROUNDS)
   bool cull = true; // FAST density: spatial j order + chunk culling (env SPH_B200_CULL=0 disables)
   DevBuf<char> dense, cub_tmp;
   PinnedBuf h_stage, h_small;
@@ -318,6 +320,7 @@ struct sph_ctx {
     items_b.release(); hcur.release(); wc.release(); rounds.release(); dense.release();
     cub_tmp.release(); h_stage.release(); h_small.release(); owned.release();
     items_c.release(); items_d2.release(); cnt_sp.release(); cnt_dn.release(); pairs_dev2.release();
+    item_ctr.release();
     items_g.release(); hdep.release(); sub_mask.release(); sub_cnt.release(); items_sub.release();
     dd_mask.release(); dd_flag.release(); dd_sel.release(); dd_cnt.release();
     mi_k.release(); mi_off.release(); mi_tmp.release();
@@ -559,11 +562,29 @@ struct sph_ctx {
       cnt_dn.ensure(ncells);
       pairs_dev2.ensure(2);
     }
-    for (int r = 0; r < 30 && (nitems > 0 || nitems_d > 0); ++r) {
+    // Device-counted rounds (lean FAST density with the dense/sparse split): rounds
+    // 1 .. kSpecRounds-1 are queued right behind round 0 without the host learning their
+    // item counts; their kernels are persistent and read the count that the previous
+    // round's make_items left in device memory (an empty round costs one short launch).
+    // The host synchronises once after round kSpecRounds-1 and continues round by round
+    // only if particles are still pending (rare: two rounds are typical at dt = 1e-4).
+    const bool spec = split && !exact && !meanw && dev_rounds;
+    constexpr int kSpecRounds = 3;
+    if (spec) {
+      item_ctr.ensure(2);
+      h_small.ensure(64 + 64 * kSpecRounds);
+    }
+    auto slot = [&](int r) { return (char *)h_small.p + 64 + 64 * r; };
+    bool host_known = true; // nitems, nitems_d, pairs, pending describe round r
+    for (int r = 0; r < 30; ++r) {
+      if (host_known && nitems <= 0 && nitems_d <= 0) break;
+      const bool devc = spec && r > 0 && r < kSpecRounds;
       A.items = items;
       A.list = list;
       A.round = r;
       A.jslices = r == 0 ? js0 : js1;
+      A.n_items_dev = devc ? scalars.p : nullptr;
+      A.item_ctr = devc ? item_ctr.p : nullptr;
       if (meanw) {
         launch_density_exact(A, nitems, use_aos, true, stream);
         launched();
@@ -572,19 +593,24 @@ struct sph_ctx {
       if (r < 4) CK(cudaEventRecord(rev[2 * r], stream));
       if (exact) launch_density_exact(A, nitems, use_aos, false, stream);
       else launch_density_fast(A, nitems, use_aos, stream);
-      if (nitems_d > 0) { // same round, dense cells, one lane per particle
+      launched();
+      if (devc || nitems_d > 0) { // same round, dense cells, one lane per particle
         DenArgs D = A;
         D.items = items_d;
         D.jslices = 1;
+        D.n_items_dev = devc ? scalars.p + 1 : nullptr;
+        D.item_ctr = devc ? item_ctr.p + 1 : nullptr;
         launch_density_fast(D, nitems_d, use_aos, stream);
         launched();
       }
       if (r < 4) CK(cudaEventRecord(rev[2 * r + 1], stream));
       launch_compact_pending(pend_out, cnt_out, list, cnt_cur, again.p, cell_begin.p, ncells,
                              stream);
-      pairs_total += pairs;
-      updates += pending;
-      max_round = r + 1;
+      if (host_known) {
+        pairs_total += pairs;
+        updates += pending;
+        max_round = r + 1;
+      }
       if (split) {
         launch_split_pending(cnt_sp.p, cnt_dn.p, cnt_out, cnt.p, den_dense_frac, ncells, stream);
         launch_make_items(items_next, scalars.p, pairs_dev.p, cnt_sp.p, cell_begin.p, na_cell.p,
@@ -592,16 +618,33 @@ struct sph_ctx {
         launch_make_items(items_next_d, scalars.p + 1, pairs_dev2.p, cnt_dn.p, cell_begin.p,
                           na_cell.p, cell_order.p, ncells, stream, kTI, items_scratch());
         launched(8);
-        CK(cudaMemcpyAsync(h_small.p, scalars.p, 2 * sizeof(int), cudaMemcpyDeviceToHost, stream));
-        CK(cudaMemcpyAsync((char *)h_small.p + 8, pairs_dev.p, 2 * sizeof(long long),
-                           cudaMemcpyDeviceToHost, stream));
-        CK(cudaMemcpyAsync((char *)h_small.p + 24, pairs_dev2.p, 2 * sizeof(long long),
-                           cudaMemcpyDeviceToHost, stream));
-        CK(cudaStreamSynchronize(stream));
-        nitems = ((int *)h_small.p)[0];
-        nitems_d = ((int *)h_small.p)[1];
-        pairs = *(long long *)((char *)h_small.p + 8) + *(long long *)((char *)h_small.p + 24);
-        pending = *(long long *)((char *)h_small.p + 16) + *(long long *)((char *)h_small.p + 32);
+        char *hs = spec && r < kSpecRounds ? slot(r) : (char *)h_small.p;
+        CK(cudaMemcpyAsync(hs, scalars.p, 2 * sizeof(int), cudaMemcpyDeviceToHost, stream));
+        CK(cudaMemcpyAsync(hs + 8, pairs_dev.p, 2 * sizeof(long long), cudaMemcpyDeviceToHost,
+                           stream));
+        CK(cudaMemcpyAsync(hs + 24, pairs_dev2.p, 2 * sizeof(long long), cudaMemcpyDeviceToHost,
+                           stream));
+        const bool queue_next = spec && r + 1 < kSpecRounds;
+        if (!queue_next) {
+          CK(cudaStreamSynchronize(stream));
+          if (spec && r + 1 == kSpecRounds) {
+            // account the device-counted rounds 1 .. r now that their counts are on the host
+            for (int k = 1; k <= r; ++k) {
+              const char *q = slot(k - 1);
+              if (((const int *)q)[0] <= 0 && ((const int *)q)[1] <= 0) break;
+              pairs_total += *(const long long *)(q + 8) + *(const long long *)(q + 24);
+              updates += *(const long long *)(q + 16) + *(const long long *)(q + 32);
+              max_round = k + 1;
+            }
+          }
+        }
+        host_known = !queue_next;
+        if (host_known) {
+          nitems = ((int *)hs)[0];
+          nitems_d = ((int *)hs)[1];
+          pairs = *(long long *)(hs + 8) + *(long long *)(hs + 24);
+          pending = *(long long *)(hs + 16) + *(long long *)(hs + 32);
+        }
       } else {
         launch_make_items(items_next, scalars.p, pairs_dev.p, cnt_out, cell_begin.p, na_cell.p,
                           cell_order.p, ncells, stream, kTI / js1, items_scratch());
@@ -614,11 +657,13 @@ struct sph_ctx {
         pairs = *(long long *)((char *)h_small.p + 8);
         pending = *(long long *)((char *)h_small.p + 16);
       }
-      if (r < 4) {
-        float ms = 0;
-        CK(cudaEventElapsedTime(&ms, rev[2 * r], rev[2 * r + 1]));
-        round_ms[r] = ms;
-      }
+      if (host_known) // the rounds since the last synchronisation have completed
+        for (int k = 0; k <= r && k < 4; ++k)
+          if (round_ms[k] == 0.0 && k < max_round) {
+            float ms = 0;
+            CK(cudaEventElapsedTime(&ms, rev[2 * k], rev[2 * k + 1]));
+            round_ms[k] = ms;
+          }
       // next round reads what this one produced
       items = items_next;
       items_d = items_next_d;
@@ -1490,6 +1535,7 @@ int sph_create(int device, sph_ctx **out) {
   if (!ctx) return SPH_E_CUDA;
   ctx->device = device;
   if (const char *e = std::getenv("SPH_B200_CULL")) ctx->cull = std::atoi(e) != 0;
+  if (const char *e = std::getenv("SPH_B200_DEV_ROUNDS")) ctx->dev_rounds = std::atoi(e) != 0;
   if (const char *e = std::getenv("SPH_B200_REBIN_FIXUP")) ctx->rebin_fixup_on = std::atoi(e);
   if (const char *e = std::getenv("SPH_B200_FORCE2")) ctx->force2 = std::atoi(e);
   if (const char *e = std::getenv("SPH_B200_PIPELINE")) ctx->pipeline = std::atoi(e);

@@ -431,6 +431,10 @@ constexpr int kF2NearU = SPH_F2_NEARU;
 #define SPH_D2_U 1 // density round-0 pair loop unroll (groups of 4 pairs; 2: +1.5 %)
 #endif
 constexpr int kD2U = SPH_D2_U;
+#ifndef SPH_D2_G
+#define SPH_D2_G 4 // density round-0 pairs per group (distance chains interleaved)
+#endif
+constexpr int kD2G = SPH_D2_G;
 #ifndef SPH_D2_JU
 #define SPH_D2_JU 4 // density j-slice (rounds >= 1) pair loop unroll (4: round 1 -1.4 %)
 #endif
@@ -854,20 +858,11 @@ __device__ __forceinline__ void density2_pair(const FastPolicy::DI &I, int hiQ05
 // tight as in round 0. Lane slice q takes j = q, q + JS, ... of each tile; the JS partial
 // sums are combined with shuffles at the end.
 
-template <int MINB, int JS, bool AOS>
-__global__ void __launch_bounds__(kD2W * 32, MINB) density2_kernel(DenArgs A) {
-  // [0], [1]: cp.async staging double buffer; [2]: the staged chunk's j's that can reach
-  // the warp (compacted), which the pair loop consumes
-  __shared__ D2Tile tiles[kD2W][3];
-  __shared__ ActiveLayout lay[kD2W];
-  const int w = warp_in_cta(), lane = lane_id(); // (a static w = 0 measured +0.6 % here)
-  const int item_idx = blockIdx.x * kD2W + w;
-  if (item_idx >= A.n_items) return;
-  if (lane < 12) {
-#pragma unroll
-    for (int b = 0; b < 3; ++b) tiles[w][b].spl[lane] = kSplPE[lane];
-  }
-  ActiveLayout &L = lay[w];
+// One work item of a density round (a cell and up to 32/JS of its pending locals).
+template <int JS, bool AOS>
+__device__ __forceinline__ void density2_item(const DenArgs &A, D2Tile (&tiles)[3],
+                                              ActiveLayout &L, int item_idx, int lane) {
+  D2Tile(&tiles_w)[3] = tiles; // this warp's staging buffers
   const Item it = A.items[item_idx];
   if (lane == 0) build_active(A.g, it.cell, L);
   const int iw = lane / JS, qs = lane % JS;
@@ -905,27 +900,27 @@ __global__ void __launch_bounds__(kD2W * 32, MINB) density2_kernel(DenArgs A) {
       const int cnb = __shfl_sync(0xffffffffu, nb, b), ck = __shfl_sync(0xffffffffu, kk, b);
       const bool has_next = todo != 0u;
       if (!staged) {
-        if constexpr (AOS) density2_stage_aos(tiles[w][buf], L, A.jlist, A.aos, cnb, ck, lane);
-        else density2_stage(tiles[w][buf], L, A.jv2, cnb, ck, lane);
+        if constexpr (AOS) density2_stage_aos(tiles_w[buf], L, A.jlist, A.aos, cnb, ck, lane);
+        else density2_stage(tiles_w[buf], L, A.jv2, cnb, ck, lane);
       }
       cp_async_wait<0>();
       __syncwarp();
       if (has_next) {
         const int bn = __ffs(todo) - 1;
         const int nnb = __shfl_sync(0xffffffffu, nb, bn), nk = __shfl_sync(0xffffffffu, kk, bn);
-        if constexpr (AOS) density2_stage_aos(tiles[w][buf ^ 1], L, A.jlist, A.aos, nnb, nk, lane);
-        else density2_stage(tiles[w][buf ^ 1], L, A.jv2, nnb, nk, lane);
+        if constexpr (AOS) density2_stage_aos(tiles_w[buf ^ 1], L, A.jlist, A.aos, nnb, nk, lane);
+        else density2_stage(tiles_w[buf ^ 1], L, A.jv2, nnb, nk, lane);
       }
       staged = has_next;
       // per-j culling: a j farther than the warp's reach from the warp box can be in no
       // lane's support (same test as chunk_near, per particle); the others are compacted
-      // into tiles[w][2], padded with inert dummies to the pair loop's granule
+      // into tiles_w[2], padded with inert dummies to the pair loop's granule
       int nj = kTJ;
-      const D2Tile *Tp = &tiles[w][buf];
+      const D2Tile *Tp = &tiles_w[buf];
       if constexpr (JS == 1) { // (rounds >= 1 with j-slices: measured slower)
-        constexpr int PADQ = JS * ((kTJ / JS) < 4 ? (kTJ / JS) : 4); // pair-loop granule
-        const D2Tile &S = tiles[w][buf];
-        D2Tile &C = tiles[w][2];
+        constexpr int PADQ = JS * ((kTJ / JS) < 4 ? (kTJ / JS) : 4); // pair-loop granule (>= kD2G)
+        const D2Tile &S = tiles_w[buf];
+        D2Tile &C = tiles_w[2];
         const float jx = (float)S.x[lane] + (float)L.sx[cnb], jy = (float)S.y[lane] + (float)L.sy[cnb];
         const float gx = fmaxf(0.0f, fmaxf(jx - ixhi, ixlo - jx));
         const float gy = fmaxf(0.0f, fmaxf(jy - iyhi, iylo - jy));
@@ -946,11 +941,23 @@ __global__ void __launch_bounds__(kD2W * 32, MINB) density2_kernel(DenArgs A) {
         }
         nj = ((nj + PADQ - 1) / PADQ) * PADQ;
         __syncwarp();
-        Tp = &tiles[w][2];
+        Tp = &tiles_w[2];
       }
       const D2Tile &T = *Tp;
       const double xs = xi.x - L.sx[cnb], ys = xi.y - L.sy[cnb]; // periodic image, i side
-      if constexpr (JS == 1) {
+      if constexpr (JS == 1 && kD2G == 2) { // pairs of pairs (fewer live registers)
+#pragma unroll kD2U
+        for (int j = 0; j < nj; j += 2) {
+          const double2 X = *reinterpret_cast<const double2 *>(&T.x[j]);
+          const double2 Y = *reinterpret_cast<const double2 *>(&T.y[j]);
+          const double dx0 = xs - X.x, dx1 = xs - X.y, dy0 = ys - Y.x, dy1 = ys - Y.y;
+          const double r20 = fma(dx0, dx0, dy0 * dy0), r21 = fma(dx1, dx1, dy1 * dy1);
+          if (in_support(r20, I.hiH2m1))
+            density2_pair(I, hiQ05, hiQ15, T, j, dx0, dy0, r20, k0375, s);
+          if (in_support(r21, I.hiH2m1))
+            density2_pair(I, hiQ05, hiQ15, T, j + 1, dx1, dy1, r21, k0375, s);
+        }
+      } else if constexpr (JS == 1) {
 #pragma unroll kD2U
         for (int j = 0; j < nj; j += 4) {
           double dx[4], dy[4], r2[4];
@@ -1028,6 +1035,37 @@ __global__ void __launch_bounds__(kD2W * 32, MINB) density2_kernel(DenArgs A) {
     A.soa.h[slot] = o[0]; A.soa.rho[slot] = o[1]; A.soa.wcount[slot] = o[2];
     A.soa.rho_dh[slot] = o[3]; A.soa.rot_v[slot] = o[4]; A.soa.div_v[slot] = o[5];
     if (st == 2) A.soa.flags[slot] += 1;
+  }
+}
+
+// A density round. With A.n_items_dev set the kernel is persistent: the round's item count
+// is read from device memory (written by the previous round's make_items) and warps take
+// items from A.item_ctr in list order, so consecutive rounds are queued without the host
+// learning the count in between (capi.cu run_density).
+template <int MINB, int JS, bool AOS>
+__global__ void __launch_bounds__(kD2W * 32, MINB) density2_kernel(DenArgs A) {
+  // [0], [1]: cp.async staging double buffer; [2]: the staged chunk's j's that can reach
+  // the warp (compacted), which the pair loop consumes
+  __shared__ D2Tile tiles[kD2W][3];
+  __shared__ ActiveLayout lay[kD2W];
+  const int w = warp_in_cta(), lane = lane_id(); // (a static w = 0 measured +0.6 % here)
+  if (lane < 12) {
+#pragma unroll
+    for (int b = 0; b < 3; ++b) tiles[w][b].spl[lane] = kSplPE[lane];
+  }
+  if (!A.n_items_dev) {
+    const int item_idx = blockIdx.x * kD2W + w;
+    if (item_idx < A.n_items) density2_item<JS, AOS>(A, tiles[w], lay[w], item_idx, lane);
+    return;
+  }
+  const int total = *A.n_items_dev;
+  for (;;) {
+    int idx = 0;
+    if (lane == 0) idx = atomicAdd(A.item_ctr, 1);
+    idx = __shfl_sync(0xffffffffu, idx, 0);
+    if (idx >= total) return;
+    density2_item<JS, AOS>(A, tiles[w], lay[w], idx, lane);
+    __syncwarp();
   }
 }
 
@@ -1156,13 +1194,20 @@ void launch_jview_force(double2 *xy, double2 *vv, double2 *mg, double2 *pv, doub
 }
 
 void launch_density_fast(const DenArgs &a, int n_items, bool aos, cudaStream_t s) {
-  if (n_items <= 0) return;
+  if (n_items <= 0 && !a.n_items_dev) return;
   DenArgs b = a;
   b.n_items = n_items;
   const int G = pair_grid(n_items), B = kWarpsPerCta * 32;
   if (b.boxes && b.jlist && b.jv2.x) {
     b.k0375 = 0.375;
-    const int G2 = (n_items + kD2W - 1) / kD2W, B2 = kD2W * 32;
+    int G2 = (n_items + kD2W - 1) / kD2W;
+    const int B2 = kD2W * 32;
+    if (b.n_items_dev) { // persistent: every resident warp slot, items taken from item_ctr
+      static int sms = 0;
+      if (!sms) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+      G2 = sms * SPH_MINB_D2 / kD2W;
+      cudaMemsetAsync(b.item_ctr, 0, sizeof(int), s);
+    }
     if (aos) {
       switch (b.jslices) {
       case 2: density2_kernel<SPH_MINB_D2, 2, true><<<G2, B2, 0, s>>>(b); break;

@@ -82,6 +82,8 @@ struct DenArgs {
   int jslices;          // density2: lanes per local particle (1, 2, 4); items hold 32/jslices
   unsigned long long *fail_count; // optional: particles that hit the 30-round limit
                                   // (density_step's Fail, kernels.cpp:190), for sph_stats
+  const int *n_items_dev; // density2: non-null = persistent launch, item count in device memory
+  int *item_ctr;          // density2 persistent launch: next item (zeroed before the launch)
 };
 
 struct ForArgs {
