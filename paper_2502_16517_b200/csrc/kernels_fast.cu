@@ -561,22 +561,10 @@ __device__ __forceinline__ void force2_convert_aos(F2Tile &T, const ActiveLayout
   }
 }
 
-template <int MINB, bool AOS>
-__global__ void __launch_bounds__(kF2W * 32, MINB) force2_kernel(F2Args A) {
-  __shared__ F2Tile tiles[kF2W][2];
-  __shared__ ActiveLayout lay[kF2W];
-  // one-warp CTAs: w = 0 statically, so the tile addresses need no thread-index arithmetic
-  // and stay cheap to rematerialise under register pressure (force sweep -4.6 %)
-  const int w = kF2W == 1 ? 0 : warp_in_cta(), lane = lane_id();
-  const int item_idx = blockIdx.x * kF2W + w;
-  if (item_idx >= A.n_items) return;
-#if SPH_F2_QH
-  if (lane < 6) tiles[w][0].spl[lane] = tiles[w][1].spl[lane] = kSplQ[lane];
-#else
-  if (lane < 9) tiles[w][0].spl[lane] = tiles[w][1].spl[lane] = kSplE[lane];
-#endif
-  if (lane == 0) tiles[w][0].edge = tiles[w][1].edge = 0;
-  ActiveLayout &L = lay[w];
+// One work item of the force sweep (a cell and up to 32 of its locals).
+template <bool AOS>
+__device__ __forceinline__ void force2_item(const F2Args &A, F2Tile (&tl)[2], ActiveLayout &L,
+                                            int item_idx, int lane) {
   const Item it = A.items[item_idx];
   if (lane == 0) build_active(A.g, it.cell, L);
   const bool live = lane < it.count;
@@ -633,27 +621,27 @@ __global__ void __launch_bounds__(kF2W * 32, MINB) force2_kernel(F2Args A) {
       // one warp barrier per chunk: after it every lane's copies of this chunk are visible
       // and every lane is done with the previous chunk, whose buffer the next staging reuses
       if (!staged) {
-        if constexpr (AOS) force2_stage_aos(tiles[w][buf], L, A.list, A.aos, cnb, ck, lane);
-        else force2_stage(tiles[w][buf], L, A.jv, cnb, ck, lane);
+        if constexpr (AOS) force2_stage_aos(tl[buf], L, A.list, A.aos, cnb, ck, lane);
+        else force2_stage(tl[buf], L, A.jv, cnb, ck, lane);
       }
       cp_async_wait<0>();
       __syncwarp();
       if constexpr (AOS) {
-        force2_convert_aos(tiles[w][buf], L, A.grav, cnb, ck, lane);
+        force2_convert_aos(tl[buf], L, A.grav, cnb, ck, lane);
         __syncwarp();
       }
       if (has_next) {
         const int bn = __ffs(todo) - 1;
         const int nnb = __shfl_sync(0xffffffffu, nb, bn), nk = __shfl_sync(0xffffffffu, kk, bn);
-        if constexpr (AOS) force2_stage_aos(tiles[w][buf ^ 1], L, A.list, A.aos, nnb, nk, lane);
-        else force2_stage(tiles[w][buf ^ 1], L, A.jv, nnb, nk, lane);
+        if constexpr (AOS) force2_stage_aos(tl[buf ^ 1], L, A.list, A.aos, nnb, nk, lane);
+        else force2_stage(tl[buf ^ 1], L, A.jv, nnb, nk, lane);
       }
       staged = has_next;
-      const F2Tile &T = tiles[w][buf];
+      const F2Tile &T = tl[buf];
       const double2 xr = xi;
       const double xs = xr.x - L.sx[cnb], ys = xr.y - L.sy[cnb]; // periodic image, i side
       if ((nmask >> b) & 1u) {
-        tiles[w][buf].vsig0[lane] = vsig;
+        tl[buf].vsig0[lane] = vsig;
 #pragma unroll kF2NearU
         for (int j = 0; j < kTJ; j += 2) {
           const double2 X = *reinterpret_cast<const double2 *>(&T.x[j]);
@@ -686,7 +674,7 @@ __global__ void __launch_bounds__(kF2W * 32, MINB) force2_kernel(F2Args A) {
         if (T.edge) { // warp-uniform after the barrier; rare
           vsig = force2_edge(I, T, lane, xi, xs, ys, hiH2m1);
           __syncwarp();
-          if (lane == 0) tiles[w][buf].edge = 0;
+          if (lane == 0) tl[buf].edge = 0;
         }
       } else {
 #pragma unroll kF2FarU
@@ -735,6 +723,36 @@ __global__ void __launch_bounds__(kF2W * 32, MINB) force2_kernel(F2Args A) {
     A.soa.u_dt[slot] = o[2];
     A.soa.v_sig[slot] = o[3];
     A.soa.h_dt[slot] = o[4];
+  }
+}
+
+// With A.item_ctr set the kernel is persistent: one warp per resident slot, items taken in
+// list order from the counter (dynamic balance instead of the hardware's CTA order).
+template <int MINB, bool AOS>
+__global__ void __launch_bounds__(kF2W * 32, MINB) force2_kernel(F2Args A) {
+  __shared__ F2Tile tiles[kF2W][2];
+  __shared__ ActiveLayout lay[kF2W];
+  // one-warp CTAs: w = 0 statically, so the tile addresses need no thread-index arithmetic
+  // and stay cheap to rematerialise under register pressure (force sweep -4.6 %)
+  const int w = kF2W == 1 ? 0 : warp_in_cta(), lane = lane_id();
+  if (!A.item_ctr && blockIdx.x * kF2W + w >= A.n_items) return;
+#if SPH_F2_QH
+  if (lane < 6) tiles[w][0].spl[lane] = tiles[w][1].spl[lane] = kSplQ[lane];
+#else
+  if (lane < 9) tiles[w][0].spl[lane] = tiles[w][1].spl[lane] = kSplE[lane];
+#endif
+  if (lane == 0) tiles[w][0].edge = tiles[w][1].edge = 0;
+  if (!A.item_ctr) {
+    force2_item<AOS>(A, tiles[w], lay[w], blockIdx.x * kF2W + w, lane);
+    return;
+  }
+  for (;;) {
+    int idx = 0;
+    if (lane == 0) idx = atomicAdd(A.item_ctr, 1);
+    idx = __shfl_sync(0xffffffffu, idx, 0);
+    if (idx >= A.n_items) return;
+    force2_item<AOS>(A, tiles[w], lay[w], idx, lane);
+    __syncwarp();
   }
 }
 
@@ -1053,12 +1071,12 @@ __global__ void __launch_bounds__(kD2W * 32, MINB) density2_kernel(DenArgs A) {
 #pragma unroll
     for (int b = 0; b < 3; ++b) tiles[w][b].spl[lane] = kSplPE[lane];
   }
-  if (!A.n_items_dev) {
+  if (!A.item_ctr) {
     const int item_idx = blockIdx.x * kD2W + w;
     if (item_idx < A.n_items) density2_item<JS, AOS>(A, tiles[w], lay[w], item_idx, lane);
     return;
   }
-  const int total = *A.n_items_dev;
+  const int total = A.n_items_dev ? *A.n_items_dev : A.n_items;
   for (;;) {
     int idx = 0;
     if (lane == 0) idx = atomicAdd(A.item_ctr, 1);
@@ -1139,7 +1157,17 @@ void launch_force2(const F2Args &a, int n_items, int n, cudaStream_t s) {
   b.n_items = n_items;
   b.k1875 = 1.875;
   b.k0375 = 0.375;
-  const int G = (n_items + kF2W - 1) / kF2W;
+  int G = (n_items + kF2W - 1) / kF2W;
+  if (b.item_ctr) { // persistent: every resident warp slot
+    static int sms = 0;
+    if (!sms) {
+      int dev = 0;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    }
+    G = std::min(G, sms * SPH_MINB_F2 / kF2W);
+    cudaMemsetAsync(b.item_ctr, 0, sizeof(int), s);
+  }
   if (aos) force2_kernel<SPH_MINB_F2, true><<<G, kF2W * 32, 0, s>>>(b);
   else force2_kernel<SPH_MINB_F2, false><<<G, kF2W * 32, 0, s>>>(b);
 }
@@ -1195,6 +1223,7 @@ void launch_jview_force(double2 *xy, double2 *vv, double2 *mg, double2 *pv, doub
 
 void launch_density_fast(const DenArgs &a, int n_items, bool aos, cudaStream_t s) {
   if (n_items <= 0 && !a.n_items_dev) return;
+  // (persistent launches: item_ctr set; the count is n_items or, if set, *n_items_dev)
   DenArgs b = a;
   b.n_items = n_items;
   const int G = pair_grid(n_items), B = kWarpsPerCta * 32;
@@ -1202,9 +1231,13 @@ void launch_density_fast(const DenArgs &a, int n_items, bool aos, cudaStream_t s
     b.k0375 = 0.375;
     int G2 = (n_items + kD2W - 1) / kD2W;
     const int B2 = kD2W * 32;
-    if (b.n_items_dev) { // persistent: every resident warp slot, items taken from item_ctr
+    if (b.item_ctr) { // persistent: every resident warp slot, items taken from item_ctr
       static int sms = 0;
-      if (!sms) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+      if (!sms) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+      }
       G2 = sms * SPH_MINB_D2 / kD2W;
       cudaMemsetAsync(b.item_ctr, 0, sizeof(int), s);
     }

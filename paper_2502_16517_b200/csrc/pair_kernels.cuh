@@ -82,8 +82,8 @@ struct DenArgs {
   int jslices;          // density2: lanes per local particle (1, 2, 4); items hold 32/jslices
   unsigned long long *fail_count; // optional: particles that hit the 30-round limit
                                   // (density_step's Fail, kernels.cpp:190), for sph_stats
-  const int *n_items_dev; // density2: non-null = persistent launch, item count in device memory
-  int *item_ctr;          // density2 persistent launch: next item (zeroed before the launch)
+  int *item_ctr;          // density2: non-null = persistent launch, warps take items from it
+  const int *n_items_dev; // density2 persistent launch: item count in device memory (else n_items)
 };
 
 struct ForArgs {
@@ -119,6 +119,7 @@ struct F2Args {
   const float4 *boxes;
   F2View jv;
   double k1875, k0375; // series constants (kernel parameters -> constant-bank operands)
+  int *item_ctr;       // non-null: persistent launch, warps take items from this counter
 };
 
 // ---- j staging (gather one active record into the SoA tile) ----
