@@ -255,8 +255,11 @@ struct sph_ctx {
   DevBuf<double2> jv2_vv;
   size_t jv_blocks() const { return (size_t)n / 32 + (size_t)ncells + 2; }
   int force2 = 1; // FAST force on the resident SoA: issue-lean kernel (env SPH_B200_FORCE2=0: old)
-  int den_js0 = 1, den_js1 = 2; // lean density: lanes per particle in round 0 / rounds >= 1
-  double den_dense_frac = 0.35;  // rounds >= 1 use one lane per particle above this pending share
+  // lean density: lanes per particle in round 0 / rounds >= 1; rounds >= 1 use one lane per
+  // particle in cells whose pending share exceeds den_dense_frac (r2, profiles/r2e_den_js1.txt:
+  // 4 lanes / 0.5 against 2 / 0.35: C2 round 1 3.89 -> 3.45 ms, C4 within 0.4 %)
+  int den_js0 = 1, den_js1 = 4;
+  double den_dense_frac = 0.5;
   bool dev_rounds = true; // density rounds >= 1 queued with device-side item counts (env SPH_B200_DEV_ROUNDS)
   // persistent pair sweeps (one warp per resident slot, items from an atomic counter in list
   // order): force -1.3 %, density round 0 -0.9 % against one CTA per item (r2d)
@@ -520,7 +523,7 @@ struct sph_ctx {
     }
     const bool lean = A.jv2.x != nullptr;
     const int js0 = lean ? std::max(1, std::min(4, den_js0)) : 1;
-    const int js1 = lean ? std::max(1, std::min(4, den_js1)) : 1;
+    const int js1 = lean ? std::max(1, std::min(8, den_js1)) : 1;
     const Item *items = items0.p;
     const int *list = ilist.p;
     const int *cnt_cur = cnt.p; // entries of `list` per cell (round 0: every local)

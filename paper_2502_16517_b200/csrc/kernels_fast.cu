@@ -1245,12 +1245,14 @@ void launch_density_fast(const DenArgs &a, int n_items, bool aos, cudaStream_t s
       switch (b.jslices) {
       case 2: density2_kernel<SPH_MINB_D2, 2, true><<<G2, B2, 0, s>>>(b); break;
       case 4: density2_kernel<SPH_MINB_D2, 4, true><<<G2, B2, 0, s>>>(b); break;
+      case 8: density2_kernel<SPH_MINB_D2, 8, true><<<G2, B2, 0, s>>>(b); break;
       default: density2_kernel<SPH_MINB_D2, 1, true><<<G2, B2, 0, s>>>(b); break;
       }
     } else {
       switch (b.jslices) {
       case 2: density2_kernel<SPH_MINB_D2, 2, false><<<G2, B2, 0, s>>>(b); break;
       case 4: density2_kernel<SPH_MINB_D2, 4, false><<<G2, B2, 0, s>>>(b); break;
+      case 8: density2_kernel<SPH_MINB_D2, 8, false><<<G2, B2, 0, s>>>(b); break;
       default: density2_kernel<SPH_MINB_D2, 1, false><<<G2, B2, 0, s>>>(b); break;
       }
     }
