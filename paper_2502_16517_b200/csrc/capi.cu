@@ -260,6 +260,8 @@ struct sph_ctx {
   // 4 lanes / 0.5 against 2 / 0.35: C2 round 1 3.89 -> 3.45 ms, C4 within 0.4 %)
   int den_js0 = 1, den_js1 = 4;
   double den_dense_frac = 0.5;
+  int den_dense_abs = 1024; // ... or whose pending count reaches this (env SPH_B200_DEN_DENSE_ABS;
+                           // C3 round 1 15.1 -> 13.2 ms, C2 and C4 unchanged, r2g)
   bool dev_rounds = true; // density rounds >= 1 queued with device-side item counts (env SPH_B200_DEV_ROUNDS)
   // persistent pair sweeps (one warp per resident slot, items from an atomic counter in list
   // order): force -1.3 %, density round 0 -0.9 % against one CTA per item (r2d)
@@ -620,7 +622,8 @@ struct sph_ctx {
         max_round = r + 1;
       }
       if (split) {
-        launch_split_pending(cnt_sp.p, cnt_dn.p, cnt_out, cnt.p, den_dense_frac, ncells, stream);
+        launch_split_pending(cnt_sp.p, cnt_dn.p, cnt_out, cnt.p, den_dense_frac, den_dense_abs, ncells,
+                             stream);
         launch_make_items(items_next, scalars.p, pairs_dev.p, cnt_sp.p, cell_begin.p, na_cell.p,
                           cell_order.p, ncells, stream, kTI / js1, items_scratch());
         launch_make_items(items_next_d, scalars.p + 1, pairs_dev2.p, cnt_dn.p, cell_begin.p,
@@ -1562,6 +1565,7 @@ int sph_create(int device, sph_ctx **out) {
   if (const char *e = std::getenv("SPH_B200_DEN_JS0")) ctx->den_js0 = std::atoi(e);
   if (const char *e = std::getenv("SPH_B200_DEN_JS1")) ctx->den_js1 = std::atoi(e);
   if (const char *e = std::getenv("SPH_B200_DEN_DENSE")) ctx->den_dense_frac = std::atof(e);
+  if (const char *e = std::getenv("SPH_B200_DEN_DENSE_ABS")) ctx->den_dense_abs = std::atoi(e);
   int r = guarded(ctx, [&] {
     CK(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
     ctx->own_stream = ctx->stream;

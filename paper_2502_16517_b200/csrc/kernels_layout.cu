@@ -701,10 +701,12 @@ __global__ void append_halo_kernel(SoaMirror f, const double *__restrict__ in, i
 
 __global__ void split_pending_kernel(int *__restrict__ sp, int *__restrict__ dn,
                                      const int *__restrict__ pend, const int *__restrict__ cnt,
-                                     double frac, int ncells) {
+                                     double frac, int dense_abs, int ncells) {
   const int c = blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= ncells) return;
-  const bool dense = (double)pend[c] > frac * (double)cnt[c];
+  // full warps stay spatially compact when the cell's pending particles are dense (share) or
+  // simply many (count: a heavy cell of a clustered box walks a long active list per item)
+  const bool dense = (double)pend[c] > frac * (double)cnt[c] || pend[c] >= dense_abs;
   sp[c] = dense ? 0 : pend[c];
   dn[c] = dense ? pend[c] : 0;
 }
@@ -1015,8 +1017,10 @@ void launch_append_halo(const SoaMirror &f_at, const double *in, int m, cudaStre
   if (m > 0) append_halo_kernel<<<(m + 255) / 256, 256, 0, s>>>(f_at, in, m);
 }
 void launch_split_pending(int *sp, int *dn, const int *pend, const int *cnt, double frac,
-                          int ncells, cudaStream_t s) {
-  if (ncells > 0) split_pending_kernel<<<(ncells + 255) / 256, 256, 0, s>>>(sp, dn, pend, cnt, frac, ncells);
+                          int dense_abs, int ncells, cudaStream_t s) {
+  if (ncells > 0)
+    split_pending_kernel<<<(ncells + 255) / 256, 256, 0, s>>>(sp, dn, pend, cnt, frac, dense_abs,
+                                                              ncells);
 }
 void launch_subset_counts(int *out, const int *cnt, const unsigned char *mask, int ncells,
                           cudaStream_t s) {

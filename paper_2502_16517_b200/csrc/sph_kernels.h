@@ -137,10 +137,10 @@ void launch_export_soa(Particle *dense, const Particle *aos, const SoaMirror &f,
                        int m, cudaStream_t s);
 void launch_export_halo(double *out, const SoaMirror &f, const int *sel, int m, cudaStream_t s);
 void launch_append_halo(const SoaMirror &f_at, const double *in, int m, cudaStream_t s);
-// density rounds >= 1: pending counts of the cells whose pending share is <= frac (sp, j-slice
-// items) and of the others (dn, one lane per particle)
+// density rounds >= 1: pending counts of the cells whose pending share is <= frac and count
+// < dense_abs (sp, j-slice items) and of the others (dn, one lane per particle)
 void launch_split_pending(int *sp, int *dn, const int *pend, const int *cnt, double frac,
-                          int ncells, cudaStream_t s);
+                          int dense_abs, int ncells, cudaStream_t s);
 void launch_subset_counts(int *out, const int *cnt, const unsigned char *mask, int ncells,
                           cudaStream_t s);
 // FP64 DFMA throughput probe
