@@ -593,8 +593,8 @@ __device__ __forceinline__ void force2_item(const F2Args &A, F2Tile (&tl)[2], Ac
   double axn = 0.0, ayn = 0.0, udt = 0.0, hdt = 0.0, vsig = -1.0;
   const float ixlo = warp_min((float)xi.x), ixhi = warp_max((float)xi.x);
   const float iylo = warp_min((float)xi.y), iyhi = warp_max((float)xi.y);
-  const float reach = warp_max((float)(2.5 * hi)) * (1.0f + 1e-5f) + 1e-6f;
-  const float reach2 = reach * reach;
+  const float reach = reach_of(warp_max((float)(2.5 * hi)));
+  const float reach2 = __fmul_rn(reach, reach);
   const double k1875 = A.k1875, k0375 = A.k0375;
   __syncwarp();
 
@@ -742,16 +742,16 @@ __global__ void __launch_bounds__(kF2W * 32, MINB) force2_kernel(F2Args A) {
   if (lane < 9) tiles[w][0].spl[lane] = tiles[w][1].spl[lane] = kSplE[lane];
 #endif
   if (lane == 0) tiles[w][0].edge = tiles[w][1].edge = 0;
-  if (!A.item_ctr) {
-    force2_item<AOS>(A, tiles[w], lay[w], blockIdx.x * kF2W + w, lane);
-    return;
-  }
-  for (;;) {
-    int idx = 0;
-    if (lane == 0) idx = atomicAdd(A.item_ctr, 1);
-    idx = __shfl_sync(0xffffffffu, idx, 0);
+  // one call site of the item body for both launch modes: two inlined copies may be compiled
+  // to differently rounded FP64 code, and the results must not depend on the launch mode
+  for (int idx = blockIdx.x * kF2W + w;;) {
+    if (A.item_ctr) {
+      if (lane == 0) idx = atomicAdd(A.item_ctr, 1);
+      idx = __shfl_sync(0xffffffffu, idx, 0);
+    }
     if (idx >= A.n_items) return;
     force2_item<AOS>(A, tiles[w], lay[w], idx, lane);
+    if (!A.item_ctr) return;
     __syncwarp();
   }
 }
@@ -895,8 +895,8 @@ __device__ __forceinline__ void density2_item(const DenArgs &A, D2Tile (&tiles)[
   FastPolicy::DA s = FastPolicy::den_zero();
   const float ixlo = warp_min((float)xi.x), ixhi = warp_max((float)xi.x);
   const float iylo = warp_min((float)xi.y), iyhi = warp_max((float)xi.y);
-  const float reach = warp_max((float)(2.5 * h)) * (1.0f + 1e-5f) + 1e-6f;
-  const float reach2 = reach * reach;
+  const float reach = reach_of(warp_max((float)(2.5 * h)));
+  const float reach2 = __fmul_rn(reach, reach);
   const double k0375 = A.k0375;
   __syncwarp();
 
@@ -942,7 +942,7 @@ __device__ __forceinline__ void density2_item(const DenArgs &A, D2Tile (&tiles)[
         const float jx = (float)S.x[lane] + (float)L.sx[cnb], jy = (float)S.y[lane] + (float)L.sy[cnb];
         const float gx = fmaxf(0.0f, fmaxf(jx - ixhi, ixlo - jx));
         const float gy = fmaxf(0.0f, fmaxf(jy - iyhi, iylo - jy));
-        const bool rel = gx * gx + gy * gy <= reach2;
+        const bool rel = box_gap2(gx, gy) <= reach2;
         const unsigned rm = __ballot_sync(0xffffffffu, rel);
         nj = __popc(rm);
         const int pos = rel ? __popc(rm & ((1u << lane) - 1u)) : nj + __popc(~rm & ((1u << lane) - 1u));
@@ -1071,18 +1071,16 @@ __global__ void __launch_bounds__(kD2W * 32, MINB) density2_kernel(DenArgs A) {
 #pragma unroll
     for (int b = 0; b < 3; ++b) tiles[w][b].spl[lane] = kSplPE[lane];
   }
-  if (!A.item_ctr) {
-    const int item_idx = blockIdx.x * kD2W + w;
-    if (item_idx < A.n_items) density2_item<JS, AOS>(A, tiles[w], lay[w], item_idx, lane);
-    return;
-  }
+  // one call site of the item body for both launch modes (see force2_kernel)
   const int total = A.n_items_dev ? *A.n_items_dev : A.n_items;
-  for (;;) {
-    int idx = 0;
-    if (lane == 0) idx = atomicAdd(A.item_ctr, 1);
-    idx = __shfl_sync(0xffffffffu, idx, 0);
+  for (int idx = blockIdx.x * kD2W + w;;) {
+    if (A.item_ctr) {
+      if (lane == 0) idx = atomicAdd(A.item_ctr, 1);
+      idx = __shfl_sync(0xffffffffu, idx, 0);
+    }
     if (idx >= total) return;
     density2_item<JS, AOS>(A, tiles[w], lay[w], idx, lane);
+    if (!A.item_ctr) return;
     __syncwarp();
   }
 }

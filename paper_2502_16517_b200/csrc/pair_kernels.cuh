@@ -320,6 +320,14 @@ __device__ __forceinline__ void chunk_locate(const ActiveLayout &L, int g, int &
 
 // Warp box (or a single point) against the FP32 box of chunk (nb, k), shifted to the
 // periodic image of stencil cell nb: true if some pair can be within `reach`.
+// The near/far classification in FP32, with every rounding explicit (no contraction left to
+// the compiler): the same item then classifies its chunks identically in every inlined copy
+// of a sweep (persistent or one CTA per item), so FAST results do not depend on scheduling.
+// reach = 2.5 max(h) (1 + 1e-5) + 1e-6 covers the FP32 rounding of the positions and boxes.
+__device__ __forceinline__ float reach_of(float r25) { return __fmaf_rn(r25, 1.0f + 1e-5f, 1e-6f); }
+__device__ __forceinline__ float box_gap2(float gx, float gy) {
+  return __fmaf_rn(gx, gx, __fmul_rn(gy, gy));
+}
 __device__ __forceinline__ bool chunk_near(const ActiveLayout &L, const float4 *boxes, int nb, int k,
                                            float xlo, float xhi, float ylo, float yhi,
                                            float reach2) {
@@ -327,7 +335,7 @@ __device__ __forceinline__ bool chunk_near(const ActiveLayout &L, const float4 *
   const float sx = (float)L.sx[nb], sy = (float)L.sy[nb];
   const float gx = fmaxf(0.0f, fmaxf(b.x + sx - xhi, xlo - (b.z + sx)));
   const float gy = fmaxf(0.0f, fmaxf(b.y + sy - yhi, ylo - (b.w + sy)));
-  return gx * gx + gy * gy <= reach2;
+  return box_gap2(gx, gy) <= reach2;
 }
 
 // Visits the chunks of the active list in order, 32 at a time: lane l evaluates chunk
@@ -400,8 +408,8 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, SPH_MINB_FOR) force_kernel(
     ixhi = warp_max((float)xi.x);
     iylo = warp_min((float)xi.y);
     iyhi = warp_max((float)xi.y);
-    const float reach = warp_max((float)(2.5 * hi)) * (1.0f + 1e-5f) + 1e-6f;
-    reach2 = reach * reach;
+    const float reach = reach_of(warp_max((float)(2.5 * hi)));
+    reach2 = __fmul_rn(reach, reach);
   }
   __syncwarp();
   const bool minimg = P::kExactOrder || !A.g.use_shift;
@@ -506,8 +514,8 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, SPH_MINB_DEN) density_cull_
   // warp bounding box and reach (dead lanes carry lane 0's particle)
   const float ixlo = warp_min((float)xi.x), ixhi = warp_max((float)xi.x);
   const float iylo = warp_min((float)xi.y), iyhi = warp_max((float)xi.y);
-  const float reach = warp_max((float)(2.5 * h)) * (1.0f + 1e-5f) + 1e-6f;
-  const float reach2 = reach * reach;
+  const float reach = reach_of(warp_max((float)(2.5 * h)));
+  const float reach2 = __fmul_rn(reach, reach);
   __syncwarp();
   const bool minimg = !A.g.use_shift;
   double2 rx, rv;
