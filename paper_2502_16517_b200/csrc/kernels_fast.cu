@@ -352,33 +352,23 @@ struct FastPolicy {
 //   * the tile keeps the gravity fields as separate x[], y[], gm[] arrays so one LDS.128
 //     serves two j's; the SPH fields are paired (vx,vy), (P,V), (c,m);
 //   * the spline piece is picked from a 3-row coefficient table in shared memory
-//     (s = c_off + sgn q, E = Horner(s)): 4 FP64 ops, no selects, no predicated
-//     correction for q < 0.5;
+//     (E = Horner in q, kSplQ): no selects, no predicated correction for q < 0.5;
 //   * the series constants come from the kernel parameters (constant-bank operands), so
 //     they are not re-materialised with IMADs inside the loop.
 // ---------------------------------------------------------------------------------------
 struct __align__(16) F2Tile {
   double x[kTJ], y[kTJ], gm[kTJ];
   double2 vv[kTJ], pv[kTJ], cm[kTJ];
-  double2 spl[9]; // spline coefficient table (kSplE), one copy per tile so rows are
-                  // addressed relative to the tile pointer
+  double2 spl[9]; // spline coefficient table (kSplQ, 6 used), one copy per tile so rows
+                  // are addressed relative to the tile pointer
   double vsig0[kTJ]; // each lane's v_sig before this chunk (force2_edge)
   int edge;          // nonzero: some lane met an edge-band pair in this chunk (force2_sph)
 };
 
-// spline table rows (outer, mid, inner): {c_off, sgn}, {e3, e2}, {e1, e0};
-// s = c_off + sgn q, E(s) = ((e3 s + e2) s + e1) s + e0 (spline.hpp:12-41 as dW = -4 N E)
-__constant__ double2 kSplE[9] = {
-    {2.5, -1.0}, {1.0, 0.0}, {0.0, 0.0},   // q in [1.5, 2.5): E = s^3,            s = 2.5 - q
-    {1.5, -1.0}, {-4.0, 3.0}, {3.0, 1.0},  // q in [0.5, 1.5): -4s^3+3s^2+3s+1,    s = 1.5 - q
-    {0.0, -1.0}, {6.0, 0.0}, {-7.5, 0.0},  // q in [0, 0.5):   6s^3 - 7.5s,        s = -q
-};
-#ifndef SPH_F2_QH
-#define SPH_F2_QH 1
-#endif
 
-// the same pieces as polynomials in q (SPH_F2_QH): E = ((a3 q + a2) q + a1) q + a0, rows of
-// two double2 {a3, a2}, {a1, a0}; saves the s = c_off - q DFMA, which reads three registers
+// spline.hpp:12-41 as dW/dq = -4 N E, E per piece (outer, mid, inner) as a polynomial in q:
+// E = ((a3 q + a2) q + a1) q + a0, rows of two double2 {a3, a2}, {a1, a0}. (Round 1 used
+// s = c_off - q; the q form saves that DFMA, which reads three registers: force -0.7 %.)
 __constant__ double2 kSplQ[6] = {
     {-1.0, 7.5}, {-18.75, 15.625}, // (2.5 - q)^3
     {4.0, -15.0}, {15.0, -1.25},   // -4 s^3 + 3 s^2 + 3 s + 1, s = 1.5 - q
@@ -434,6 +424,7 @@ constexpr int kD2U = SPH_D2_U;
 #ifndef SPH_D2_G
 #define SPH_D2_G 4 // density round-0 pairs per group (distance chains interleaved)
 #endif
+
 constexpr int kD2G = SPH_D2_G;
 #ifndef SPH_D2_JU
 #define SPH_D2_JU 4 // density j-slice (rounds >= 1) pair loop unroll (4: round 1 -1.4 %)
@@ -449,30 +440,20 @@ struct F2I { double vx, vy, inv_hi, pri, mb3; int hiQ05, hiQ15; };
 // an extra live register makes ptxas rematerialise the tile address in every block, +5 %);
 // force2_edge then redoes the flagged chunk's v_sig max from the value saved before it,
 // taking edge pairs only where the reference would. The SPH block stays branch-free.
-__device__ __forceinline__ double force2_sph(const F2I &I, const F2Tile &T, int j, double dx,
-                                             double dy, double r2, double k0375, double &udt,
-                                             double &hdt, double &vsig, unsigned hiH2m1) {
+__device__ __forceinline__ double f2_rinv(double r2, double k0375) {
+  const double y0 = rsqrt_seed(r2);
+  const double e = fma(-r2, y0 * y0, 1.0);
+  return fma(y0, e * fma(e, k0375, 0.5), y0);
+}
+__device__ __forceinline__ double force2_sph_r(const F2I &I, const F2Tile &T, int j, double dx,
+                                               double dy, double r2, double rinv, double &udt,
+                                               double &hdt, double &vsig, unsigned hiH2m1) {
   const int hr = __double2hiint(r2);
-#if SPH_F2_QH
   int row = hr < I.hiQ15 ? 2 : 0;
   if (hr < I.hiQ05) row = 4;
   const double2 t1 = T.spl[row], t2 = T.spl[row + 1];
-  const double y0 = rsqrt_seed(r2);
-  const double e = fma(-r2, y0 * y0, 1.0);
-  const double rinv = fma(y0, e * fma(e, k0375, 0.5), y0);
   const double q = (r2 * rinv) * I.inv_hi;
   const double E = fma(fma(fma(t1.x, q, t1.y), q, t2.x), q, t2.y);
-#else
-  int row = hr < I.hiQ15 ? 3 : 0;
-  if (hr < I.hiQ05) row = 6;
-  const double c_off = T.spl[row].x;
-  const double2 t1 = T.spl[row + 1], t2 = T.spl[row + 2];
-  const double y0 = rsqrt_seed(r2);
-  const double e = fma(-r2, y0 * y0, 1.0);
-  const double rinv = fma(y0, e * fma(e, k0375, 0.5), y0);
-  const double s = fma(-(r2 * rinv), I.inv_hi, c_off);
-  const double E = fma(fma(fma(t1.x, s, t1.y), s, t2.x), s, t2.y);
-#endif
   const double g = E * rinv;
   const double2 vj = T.vv[j];
   const double dvx = I.vx - vj.x, dvy = I.vy - vj.y;
@@ -487,6 +468,12 @@ __device__ __forceinline__ double force2_sph(const F2I &I, const F2Tile &T, int 
   if (__double_as_longlong(vs) > __double_as_longlong(vsig)) vsig = vs;
   if ((unsigned)hr >= hiH2m1) const_cast<F2Tile &>(T).edge = hr;
   return fma(cm.y, I.pri, pv.x) * g;
+}
+
+__device__ __forceinline__ double force2_sph(const F2I &I, const F2Tile &T, int j, double dx,
+                                             double dy, double r2, double k0375, double &udt,
+                                             double &hdt, double &vsig, unsigned hiH2m1) {
+  return force2_sph_r(I, T, j, dx, dy, r2, f2_rinv(r2, k0375), udt, hdt, vsig, hiH2m1);
 }
 
 // A flagged chunk's v_sig max redone from the value before it (kernels.cpp:124-151): the
@@ -736,11 +723,7 @@ __global__ void __launch_bounds__(kF2W * 32, MINB) force2_kernel(F2Args A) {
   // and stay cheap to rematerialise under register pressure (force sweep -4.6 %)
   const int w = kF2W == 1 ? 0 : warp_in_cta(), lane = lane_id();
   if (!A.item_ctr && blockIdx.x * kF2W + w >= A.n_items) return;
-#if SPH_F2_QH
   if (lane < 6) tiles[w][0].spl[lane] = tiles[w][1].spl[lane] = kSplQ[lane];
-#else
-  if (lane < 9) tiles[w][0].spl[lane] = tiles[w][1].spl[lane] = kSplE[lane];
-#endif
   if (lane == 0) tiles[w][0].edge = tiles[w][1].edge = 0;
   // one call site of the item body for both launch modes: two inlined copies may be compiled
   // to differently rounded FP64 code, and the results must not depend on the launch mode
@@ -835,19 +818,36 @@ __device__ __forceinline__ void density2_stage_aos(D2Tile &T, const ActiveLayout
 // (the piece comes from r2 against per-i thresholds (0.5h)^2, (1.5h)^2 on the high words,
 // so the coefficient loads issue before the rsqrt chain; a pair within 2^-20 of a knot may
 // take the neighbouring piece, which agrees there to O(dq^3))
-__device__ __forceinline__ void density2_pair(const FastPolicy::DI &I, int hiQ05, int hiQ15,
-                                              const D2Tile &T, int j, double dx, double dy,
-                                              double r2, double k0375, FastPolicy::DA &s) {
+// x^-1/2 of a pair's r^2 and the derived r and q (the in-support block's head)
+struct D2Geo { double rinv, r, q; };
+__device__ __forceinline__ D2Geo density2_geo(const FastPolicy::DI &I, double r2, double k0375) {
+  const double y0 = rsqrt_seed(r2);
+  const double e = fma(-r2, y0 * y0, 1.0);
+  D2Geo G;
+  G.rinv = fma(y0, e * fma(e, k0375, 0.5), y0);
+  G.r = r2 * G.rinv;
+#if SPH_D2_QH
+  G.q = G.r * I.inv_h;
+#else
+  G.q = 0.0;
+#endif
+  return G;
+}
+
+// density_pair (kernels.cpp:97-119) for one in-support pair, on FastPolicy's scaled sums, from
+// its geometry (the piece comes from r2 against per-i thresholds (0.5h)^2, (1.5h)^2 on the
+// high words, so the coefficient loads issue early; a pair within 2^-20 of a knot may take
+// the neighbouring piece, which agrees there to O(dq^3))
+__device__ __forceinline__ void density2_acc(const FastPolicy::DI &I, int hiQ05, int hiQ15,
+                                             const D2Tile &T, int j, double dx, double dy,
+                                             double r2, const D2Geo &G, FastPolicy::DA &s) {
   const int hr = __double2hiint(r2);
   int row = hr < hiQ15 ? 4 : 0; // q < 1.5
   if (hr < hiQ05) row = 8;      // q < 0.5
   const double2 t1 = T.spl[row], t2 = T.spl[row + 1], t3 = T.spl[row + 2];
-  const double y0 = rsqrt_seed(r2);
-  const double e = fma(-r2, y0 * y0, 1.0);
-  const double rinv = fma(y0, e * fma(e, k0375, 0.5), y0);
-  const double r = r2 * rinv;
+  const double rinv = G.rinv, r = G.r;
 #if SPH_D2_QH
-  const double sv = r * I.inv_h; // q
+  const double sv = G.q; // q
 #else
   const double sv = fma(-r, I.inv_h, t3.x); // c_off - q
 #endif
@@ -864,6 +864,12 @@ __device__ __forceinline__ void density2_pair(const FastPolicy::DI &I, int hiQ05
   const double dvx = I.vx - vj.x, dvy = I.vy - vj.y;
   s.div = fma(fac, fma(dvx, dx, dvy * dy), s.div);
   s.rot = fma(fac, fma(dvx, dy, -dvy * dx), s.rot);
+}
+
+__device__ __forceinline__ void density2_pair(const FastPolicy::DI &I, int hiQ05, int hiQ15,
+                                              const D2Tile &T, int j, double dx, double dy,
+                                              double r2, double k0375, FastPolicy::DA &s) {
+  density2_acc(I, hiQ05, hiQ15, T, j, dx, dy, r2, density2_geo(I, r2, k0375), s);
 }
 
 #ifndef SPH_MINB_D2

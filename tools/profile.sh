@@ -10,8 +10,8 @@ ncu --set full --clock-control none --import-source on -k regex:^force2_kernel -
     -o gpurun_out/force_$TAG $B > /dev/null 2>&1
 # density round 0 of the second step: the first density2_kernel<20, 1, 0> launch of each
 # step is round 0 (then the dense-cell launches of rounds 1 and 2 follow under the same name)
-ncu --set full --clock-control none --import-source on --kernel-name-base demangled \
-    -k "regex:density2_kernel<20, 1, 0>" -s 3 -c 1 \
+ncu --set full --clock-control none --import-source on --kernel-name-base mangled \
+    -k "regex:density2_kernelILi20ELi1ELb0E" -s 3 -c 1 \
     -o gpurun_out/density_$TAG $B > /dev/null 2>&1
 ncu --set full --clock-control none --import-source on \
     -k regex:"^kick2_kernel|^drift_kernel|^kick1_kernel" -s 3 -c 3 -o gpurun_out/linear_$TAG $B > /dev/null 2>&1
