@@ -5,7 +5,7 @@
 // builds the reference's soaview_sph library with this file in place of kernels.cpp (and
 // links libsph_b200.so) runs its existing callers unchanged on the B200: run_bench /
 // to_csv (bench.cpp:135-233), make_particles (grid.cpp:136,141), the test suite
-// (tests/test_sph.cpp) and the CLI. INTEGRATION.md §3 shows the build change.
+// (tests/test_sph.cpp) and the CLI. INTEGRATION.md §2b shows the build change.
 //
 //   run_sweep      kernels.hpp:45-46  -> sph_bind (when the grid's lists changed) + sph_run_sweep
 //   drift_one ...  kernels.hpp:52-54  -> sph_apply_records (one record, exact kernel)
