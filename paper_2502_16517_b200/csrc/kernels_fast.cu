@@ -476,6 +476,7 @@ __device__ __forceinline__ double force2_sph(const F2I &I, const F2Tile &T, int 
   return force2_sph_r(I, T, j, dx, dy, r2, f2_rinv(r2, k0375), udt, hdt, vsig, hiH2m1);
 }
 
+
 // A flagged chunk's v_sig max redone from the value before it (kernels.cpp:124-151): the
 // pairs certainly inside with force2_sph's arithmetic, the edge-band pairs only if the
 // reference's support decision, from the unshifted positions, has them inside.
