@@ -269,8 +269,12 @@ struct sph_ctx {
   bool f2_persist = true; // force2 (env SPH_B200_F2_PERSIST)
   bool cull = true; // FAST density: spatial j order + chunk culling (env SPH_B200_CULL=0 disables)
   DevBuf<char> dense, cub_tmp;
-  PinnedBuf h_stage, h_small;
-  int n_items0 = 0;
+  PinnedBuf h_stage, h_small, h_items0;
+  int n_items0 = 0;         // valid on the host after sync_items0()
+  bool items0_pending = false; // the round-0 work list's count / pairs still in flight to the host
+  bool force_pairs_pending = false;
+  DevBuf<int> items0_n;        // its item count on the device (persistent sweeps read it there)
+  DevBuf<long long> pairs0_dev; // {sum nl*na, listed particles} of the round-0 list
   bool need_rebin = false; // particles were appended: cell lists stale until sph_rebin
   DevBuf<unsigned char> dd_mask, dd_flag, sub_mask;
   DevBuf<int> sub_cnt;
@@ -329,6 +333,7 @@ struct sph_ctx {
     cell_order.release(); cell_order_in.release(); items0.release(); items_a.release();
     items_b.release(); hcur.release(); wc.release(); rounds.release(); dense.release();
     cub_tmp.release(); h_stage.release(); h_small.release(); owned.release();
+    items0_n.release(); pairs0_dev.release(); h_items0.release();
     items_c.release(); items_d2.release(); cnt_sp.release(); cnt_dn.release(); pairs_dev2.release();
     item_ctr.release(); f2_ctr.release();
     items_g.release(); hdep.release(); sub_mask.release(); sub_cnt.release(); items_sub.release();
@@ -456,17 +461,31 @@ struct sph_ctx {
     }
     const bool aos_src = !soa_ahead;
     launch_spatial_order(ilist.p, aos.p, soa, aos_src, cell_begin.p, ncells, nx, ny, stream);
-    launch_make_items(items0.p, scalars.p, pairs_dev.p, cnt.p, cell_begin.p, na_cell.p,
+    items0_n.ensure(1);
+    pairs0_dev.ensure(2);
+    h_items0.ensure(32);
+    launch_make_items(items0.p, items0_n.p, pairs0_dev.p, cnt.p, cell_begin.p, na_cell.p,
                       cell_order.p, ncells, stream, kTI, items_scratch());
     launched(3);
-    CK(cudaMemcpyAsync(h_small.p, scalars.p, sizeof(int), cudaMemcpyDeviceToHost, stream));
-    CK(cudaMemcpyAsync((char *)h_small.p + 8, pairs_dev.p, 2 * sizeof(long long),
+    // the count travels to the host behind the step's work: the persistent density round 0
+    // and force sweep read it on the device, everything else calls sync_items0() first
+    CK(cudaMemcpyAsync(h_items0.p, items0_n.p, sizeof(int), cudaMemcpyDeviceToHost, stream));
+    CK(cudaMemcpyAsync((char *)h_items0.p + 8, pairs0_dev.p, 2 * sizeof(long long),
                        cudaMemcpyDeviceToHost, stream));
+    items0_pending = true;
+  }
+
+  // The round-0 work list's count and pair totals on the host (synchronises the stream if
+  // they are still in flight).
+  void sync_items0() {
+    if (!items0_pending) return;
     CK(cudaStreamSynchronize(stream));
-    n_items0 = *(int *)h_small.p;
-    active_pairs = *(long long *)((char *)h_small.p + 8);
-    listed0 = *(long long *)((char *)h_small.p + 16);
+    n_items0 = *(const int *)h_items0.p;
+    active_pairs = *(const long long *)((const char *)h_items0.p + 8);
+    listed0 = *(const long long *)((const char *)h_items0.p + 16);
     stats.active_pairs = active_pairs;
+    if (force_pairs_pending) stats.force_pairs = active_pairs;
+    items0_pending = force_pairs_pending = false;
   }
 
   // ---- mirror coherence ----
@@ -524,6 +543,11 @@ struct sph_ctx {
       launched();
     }
     const bool lean = A.jv2.x != nullptr;
+    // device-counted rounds (see below) and a persistent round 0 that reads its item count on
+    // the device: no host synchronisation between the rebin and the end of round 2
+    const bool spec = lean && den_js1 > 1 && !exact && !meanw && dev_rounds;
+    const bool dev0 = spec && persist0 && den_js0 <= 1;
+    if (!dev0) sync_items0();
     const int js0 = lean ? std::max(1, std::min(4, den_js0)) : 1;
     const int js1 = lean ? std::max(1, std::min(8, den_js1)) : 1;
     const Item *items = items0.p;
@@ -578,14 +602,13 @@ struct sph_ctx {
     // round's make_items left in device memory (an empty round costs one short launch).
     // The host synchronises once after round kSpecRounds-1 and continues round by round
     // only if particles are still pending (rare: two rounds are typical at dt = 1e-4).
-    const bool spec = split && !exact && !meanw && dev_rounds;
     constexpr int kSpecRounds = 3;
     item_ctr.ensure(2);
     if (spec) {
       h_small.ensure(64 + 64 * kSpecRounds);
     }
     auto slot = [&](int r) { return (char *)h_small.p + 64 + 64 * r; };
-    bool host_known = true; // nitems, nitems_d, pairs, pending describe round r
+    bool host_known = !dev0; // nitems, nitems_d, pairs, pending describe round r
     for (int r = 0; r < 30; ++r) {
       if (host_known && nitems <= 0 && nitems_d <= 0) break;
       const bool devc = spec && r > 0 && r < kSpecRounds;
@@ -593,7 +616,7 @@ struct sph_ctx {
       A.list = list;
       A.round = r;
       A.jslices = r == 0 ? js0 : js1;
-      A.n_items_dev = devc ? scalars.p : nullptr;
+      A.n_items_dev = devc ? scalars.p : (r == 0 && dev0) ? items0_n.p : nullptr;
       A.item_ctr = devc || (r == 0 && persist0 && lean && !exact && !meanw) ? item_ctr.p : nullptr;
       if (meanw) {
         launch_density_exact(A, nitems, use_aos, true, stream);
@@ -639,7 +662,15 @@ struct sph_ctx {
         if (!queue_next) {
           CK(cudaStreamSynchronize(stream));
           if (spec && r + 1 == kSpecRounds) {
-            // account the device-counted rounds 1 .. r now that their counts are on the host
+            // account the device-counted rounds 0 .. r now that their counts are on the host
+            if (dev0) {
+              sync_items0(); // (the stream is idle: no wait)
+              if (n_items0 > 0) {
+                pairs_total += active_pairs;
+                updates += listed0;
+                max_round = 1;
+              }
+            }
             for (int k = 1; k <= r; ++k) {
               const char *q = slot(k - 1);
               if (((const int *)q)[0] <= 0 && ((const int *)q)[1] <= 0) break;
@@ -699,7 +730,10 @@ struct sph_ctx {
 
   void run_force(bool use_aos, bool exact, const Params &par, const Item *items = nullptr,
                  int nitems = -1) {
+    const bool dev_count = !items && items0_pending && f2_persist && !exact && cull && force2 &&
+                           geom().use_shift;
     if (!items) {
+      if (!dev_count) sync_items0();
       items = items0.p;
       nitems = n_items0;
     }
@@ -728,9 +762,11 @@ struct sph_ctx {
         f2_ctr.ensure(2);
         B.item_ctr = f2_ctr.p;
       }
+      if (dev_count) B.n_items_dev = items0_n.p; // persistent: the count is read on the device
       launch_force2(B, nitems, (int)n, stream);
       launched(3);
-      stats.force_pairs = active_pairs;
+      if (dev_count) force_pairs_pending = true;
+      else stats.force_pairs = active_pairs;
       return;
     }
     if (!exact && cull) { // spatial j order + far-chunk gravity-only path
@@ -1297,7 +1333,8 @@ struct sph_ctx {
     CK(cudaMemcpyAsync(host_idx.p, hid.data(), sizeof(int) * n, cudaMemcpyHostToDevice, stream));
     CK(cudaMemcpyAsync(all_rank.p, ar.data(), sizeof(long long) * n, cudaMemcpyHostToDevice, stream));
     upload_full(recs);
-    rebuild_worklist(); // synchronises (host vectors above stay alive until then)
+    rebuild_worklist();
+    sync_items0(); // (host vectors above stay alive until here)
     bound = true;
     stats = sph_stats{};
     stats.n = n;
@@ -1947,6 +1984,12 @@ int sph_make_particles_ex(sph_ctx *ctx, int64_t n, int ppc, uint64_t seed, int k
 
 int sph_get_stats(const sph_ctx *ctx, sph_stats *out) {
   if (!ctx || !out) return SPH_E_ARG;
+  // counts that may still be in flight to the host (round-0 work list)
+  int r = guarded(const_cast<sph_ctx *>(ctx), [&] {
+    const_cast<sph_ctx *>(ctx)->sync_items0();
+    return SPH_OK;
+  });
+  if (r != SPH_OK) return r;
   *out = ctx->stats;
   out->layout = ctx->layout;
   out->numerics = ctx->numerics;

@@ -723,7 +723,8 @@ __global__ void __launch_bounds__(kF2W * 32, MINB) force2_kernel(F2Args A) {
   // one-warp CTAs: w = 0 statically, so the tile addresses need no thread-index arithmetic
   // and stay cheap to rematerialise under register pressure (force sweep -4.6 %)
   const int w = kF2W == 1 ? 0 : warp_in_cta(), lane = lane_id();
-  if (!A.item_ctr && blockIdx.x * kF2W + w >= A.n_items) return;
+  const int total = A.n_items_dev ? *A.n_items_dev : A.n_items;
+  if (!A.item_ctr && blockIdx.x * kF2W + w >= total) return;
   if (lane < 6) tiles[w][0].spl[lane] = tiles[w][1].spl[lane] = kSplQ[lane];
   if (lane == 0) tiles[w][0].edge = tiles[w][1].edge = 0;
   // one call site of the item body for both launch modes: two inlined copies may be compiled
@@ -733,7 +734,7 @@ __global__ void __launch_bounds__(kF2W * 32, MINB) force2_kernel(F2Args A) {
       if (lane == 0) idx = atomicAdd(A.item_ctr, 1);
       idx = __shfl_sync(0xffffffffu, idx, 0);
     }
-    if (idx >= A.n_items) return;
+    if (idx >= total) return;
     force2_item<AOS>(A, tiles[w], lay[w], idx, lane);
     if (!A.item_ctr) return;
     __syncwarp();
@@ -1157,7 +1158,7 @@ void launch_force2(const F2Args &a, int n_items, int n, cudaStream_t s) {
   if (n > 0 && a.g.ncells > 0 && !aos)
     jview_force2_kernel<false><<<a.g.ncells, 128, 0, s>>>(const_cast<double *>(a.jv.blk), a.list,
                                                           a.g.cell_begin, a.aos, a.soa, a.grav);
-  if (n_items <= 0) return;
+  if (n_items <= 0 && !a.n_items_dev) return;
   F2Args b = a;
   b.n_items = n_items;
   b.k1875 = 1.875;
@@ -1170,7 +1171,7 @@ void launch_force2(const F2Args &a, int n_items, int n, cudaStream_t s) {
       cudaGetDevice(&dev);
       cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     }
-    G = std::min(G, sms * SPH_MINB_F2 / kF2W);
+    G = b.n_items_dev ? sms * SPH_MINB_F2 / kF2W : std::min(G, sms * SPH_MINB_F2 / kF2W);
     cudaMemsetAsync(b.item_ctr, 0, sizeof(int), s);
   }
   if (aos) force2_kernel<SPH_MINB_F2, true><<<G, kF2W * 32, 0, s>>>(b);

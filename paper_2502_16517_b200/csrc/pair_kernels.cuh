@@ -120,6 +120,7 @@ struct F2Args {
   F2View jv;
   double k1875, k0375; // series constants (kernel parameters -> constant-bank operands)
   int *item_ctr;       // non-null: persistent launch, warps take items from this counter
+  const int *n_items_dev; // persistent launch: the item count in device memory (else n_items)
 };
 
 // ---- j staging (gather one active record into the SoA tile) ----
