@@ -944,7 +944,7 @@ __device__ __forceinline__ void density2_item(const DenArgs &A, D2Tile (&tiles)[
       int nj = kTJ;
       const D2Tile *Tp = &tiles_w[buf];
       if constexpr (JS == 1) { // (rounds >= 1 with j-slices: measured slower)
-        constexpr int PADQ = JS * ((kTJ / JS) < 4 ? (kTJ / JS) : 4); // pair-loop granule (>= kD2G)
+        constexpr int PADQ = JS * ((kTJ / JS) < 4 ? (kTJ / JS) : 4); // pair-loop granule
         const D2Tile &S = tiles_w[buf];
         D2Tile &C = tiles_w[2];
         const float jx = (float)S.x[lane] + (float)L.sx[cnb], jy = (float)S.y[lane] + (float)L.sy[cnb];
@@ -971,19 +971,7 @@ __device__ __forceinline__ void density2_item(const DenArgs &A, D2Tile (&tiles)[
       }
       const D2Tile &T = *Tp;
       const double xs = xi.x - L.sx[cnb], ys = xi.y - L.sy[cnb]; // periodic image, i side
-      if constexpr (JS == 1 && kD2G == 2) { // pairs of pairs (fewer live registers)
-#pragma unroll kD2U
-        for (int j = 0; j < nj; j += 2) {
-          const double2 X = *reinterpret_cast<const double2 *>(&T.x[j]);
-          const double2 Y = *reinterpret_cast<const double2 *>(&T.y[j]);
-          const double dx0 = xs - X.x, dx1 = xs - X.y, dy0 = ys - Y.x, dy1 = ys - Y.y;
-          const double r20 = fma(dx0, dx0, dy0 * dy0), r21 = fma(dx1, dx1, dy1 * dy1);
-          if (in_support(r20, I.hiH2m1))
-            density2_pair(I, hiQ05, hiQ15, T, j, dx0, dy0, r20, k0375, s);
-          if (in_support(r21, I.hiH2m1))
-            density2_pair(I, hiQ05, hiQ15, T, j + 1, dx1, dy1, r21, k0375, s);
-        }
-      } else if constexpr (JS == 1) {
+      if constexpr (JS == 1) {
 #pragma unroll kD2U
         for (int j = 0; j < nj; j += 4) {
           double dx[4], dy[4], r2[4];
