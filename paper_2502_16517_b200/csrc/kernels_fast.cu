@@ -421,11 +421,6 @@ constexpr int kF2NearU = SPH_F2_NEARU;
 #define SPH_D2_U 1 // density round-0 pair loop unroll (groups of 4 pairs; 2: +1.5 %)
 #endif
 constexpr int kD2U = SPH_D2_U;
-#ifndef SPH_D2_G
-#define SPH_D2_G 4 // density round-0 pairs per group (distance chains interleaved)
-#endif
-
-constexpr int kD2G = SPH_D2_G;
 #ifndef SPH_D2_JU
 #define SPH_D2_JU 4 // density j-slice (rounds >= 1) pair loop unroll (4: round 1 -1.4 %)
 #endif
