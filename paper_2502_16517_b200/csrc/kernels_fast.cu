@@ -1134,6 +1134,16 @@ __global__ void jview_force2_kernel(double *blk, const int *ilist, const int *ce
   }
 }
 
+// SMs of the current device (persistent launches size their grid by it; cached per device)
+static int sm_count() {
+  static int cache[64] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) dev = 0;
+  if (!cache[dev]) cudaDeviceGetAttribute(&cache[dev], cudaDevAttrMultiProcessorCount, dev);
+  return cache[dev] > 0 ? cache[dev] : 148;
+}
+
 void launch_force2(const F2Args &a, int n_items, int n, cudaStream_t s) {
   const bool aos = a.aos != nullptr;
   // the SoA layouts read the per-sweep chunk-major j-view; the AoS arm stages j's from the
@@ -1148,12 +1158,7 @@ void launch_force2(const F2Args &a, int n_items, int n, cudaStream_t s) {
   b.k0375 = 0.375;
   int G = (n_items + kF2W - 1) / kF2W;
   if (b.item_ctr) { // persistent: every resident warp slot
-    static int sms = 0;
-    if (!sms) {
-      int dev = 0;
-      cudaGetDevice(&dev);
-      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    }
+    const int sms = sm_count();
     G = b.n_items_dev ? sms * SPH_MINB_F2 / kF2W : std::min(G, sms * SPH_MINB_F2 / kF2W);
     cudaMemsetAsync(b.item_ctr, 0, sizeof(int), s);
   }
@@ -1221,13 +1226,7 @@ void launch_density_fast(const DenArgs &a, int n_items, bool aos, cudaStream_t s
     int G2 = (n_items + kD2W - 1) / kD2W;
     const int B2 = kD2W * 32;
     if (b.item_ctr) { // persistent: every resident warp slot, items taken from item_ctr
-      static int sms = 0;
-      if (!sms) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-      }
-      G2 = sms * SPH_MINB_D2 / kD2W;
+      G2 = sm_count() * SPH_MINB_D2 / kD2W;
       cudaMemsetAsync(b.item_ctr, 0, sizeof(int), s);
     }
     if (aos) {
