@@ -15,7 +15,7 @@
 // Path selects the device layout (AosBaseline -> AoS in place, SoaView -> per-call
 // AoS->SoA conversion); Order / Guard / threads do not change results (the reference's
 // variants are bitwise-equivalent, test_sph.cpp:308-346). The CellGrid is flattened and
-// bound once and re-bound when its lists change (cheap signature check per call).
+// bound once and re-bound when its lists change (an O(n) compare of the pointer lists per call).
 #pragma once
 
 #include <cstdint>
@@ -41,8 +41,7 @@ public:
   void set_layout(int layout) { check(sph_set_layout(ctx_, layout)); }
 
   void bind(const CellGrid &g) {
-    uint64_t sig = signature(g);
-    if (bound_ == &g && sig == sig_) return;
+    if (bound_ == &g && same_lists(g)) return;
     recs_.clear();
     cell_begin_.assign(1, 0);
     for (const auto &l : g.local) {
@@ -70,7 +69,6 @@ public:
     check(sph_bind(ctx_, reinterpret_cast<void *const *>(recs_.data()), cell_begin_.data(), g.nx,
                    g.ny, g.cell_size, nullptr));
     bound_ = &g;
-    sig_ = sig;
   }
 
   void *const *records() const { return reinterpret_cast<void *const *>(recs_.data()); }
@@ -86,20 +84,23 @@ private:
     if (sph_create(device, &ctx_) != SPH_OK || !ctx_)
       throw std::runtime_error("libsph_b200: no usable CUDA device");
   }
-  // Every pointer of every local list, in order: a rebuilt grid at the same address whose
-  // particles swapped cells (or were reordered) behind unchanged list sizes re-binds.
-  // run_sweep walks all n pointers to pack the upload anyway, so this is O(n) of the same.
-  static uint64_t signature(const CellGrid &g) {
-    uint64_t h = 1469598103934665603ULL ^ static_cast<uint64_t>(g.nx * 131 + g.ny);
-    for (const auto &l : g.local) {
-      h = (h ^ l.size()) * 1099511628211ULL;
-      for (const Particle *p : l) h = (h ^ reinterpret_cast<uintptr_t>(p)) * 1099511628211ULL;
+  // Every pointer of every local list, in order, against the bound copy: a rebuilt grid at
+  // the same address whose particles swapped cells (or were reordered) behind unchanged
+  // list sizes re-binds. run_sweep walks all n pointers to pack the upload anyway, so this
+  // is O(n) of the same (an exact compare, not a hash).
+  bool same_lists(const CellGrid &g) const {
+    if (g.local.size() + 1 != cell_begin_.size()) return false;
+    size_t k = 0;
+    for (size_t c = 0; c < g.local.size(); ++c) {
+      const auto &l = g.local[c];
+      if (static_cast<int64_t>(k + l.size()) != cell_begin_[c + 1]) return false;
+      for (const Particle *p : l)
+        if (recs_[k++] != p) return false;
     }
-    return h;
+    return true;
   }
   sph_ctx *ctx_ = nullptr;
   const CellGrid *bound_ = nullptr;
-  uint64_t sig_ = 0;
   std::vector<Particle *> recs_;
   std::vector<int64_t> cell_begin_;
 };
