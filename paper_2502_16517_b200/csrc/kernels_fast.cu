@@ -752,12 +752,9 @@ struct __align__(16) D2Tile {
 // E = P'(s) / 4, evaluated by the derivative Horner recursion alongside P: four table loads
 // instead of six, the same seven DFMA. Sums over m E carry the factor 4, removed at publish.
 // Rows are 4 entries apart; s = c_off - q on every piece.
-#ifndef SPH_D2_QH
-#define SPH_D2_QH 1
-#endif
 
-#if SPH_D2_QH
-// P as polynomials in q (SPH_D2_QH), rows {p4, p3}, {p2, p1}, {-, p0}: the same pieces,
+
+// spline.hpp:12-41, P per piece as a polynomial in q (round 1 used s = c_off - q), rows {p4, p3}, {p2, p1}, {-, p0}: the same pieces,
 // (2.5-q)^4, (2.5-q)^4 - 5 (1.5-q)^4, ... + 10 (0.5-q)^4, expanded (exact binary
 // coefficients); dP/dq = -4 E, so the sums over m dP/dq carry the factor -4
 __constant__ double2 kSplPE[12] = {
@@ -765,13 +762,6 @@ __constant__ double2 kSplPE[12] = {
     {-4.0, 20.0}, {-30.0, 5.0}, {0.0, 13.75}, {0.0, 0.0},
     {6.0, 0.0}, {-15.0, 0.0}, {0.0, 14.375}, {0.0, 0.0},
 };
-#else
-__constant__ double2 kSplPE[12] = {
-    {1.0, 0.0}, {0.0, 0.0}, {2.5, 0.0}, {0.0, 0.0},       // s^4,                     s = 2.5 - q
-    {-4.0, 4.0}, {6.0, 4.0}, {1.5, 1.0}, {0.0, 0.0},      // -4s^4+4s^3+6s^2+4s+1,    s = 1.5 - q
-    {6.0, 0.0}, {-15.0, 0.0}, {0.0, 14.375}, {0.0, 0.0},  // 6s^4-15s^2+14.375,       s = -q
-};
-#endif
 
 __device__ __forceinline__ void density2_stage(D2Tile &T, const ActiveLayout &L, const D2View &jv,
                                                int nb, int k, int lane) {
@@ -823,11 +813,7 @@ __device__ __forceinline__ D2Geo density2_geo(const FastPolicy::DI &I, double r2
   D2Geo G;
   G.rinv = fma(y0, e * fma(e, k0375, 0.5), y0);
   G.r = r2 * G.rinv;
-#if SPH_D2_QH
   G.q = G.r * I.inv_h;
-#else
-  G.q = 0.0;
-#endif
   return G;
 }
 
@@ -843,11 +829,7 @@ __device__ __forceinline__ void density2_acc(const FastPolicy::DI &I, int hiQ05,
   if (hr < hiQ05) row = 8;      // q < 0.5
   const double2 t1 = T.spl[row], t2 = T.spl[row + 1], t3 = T.spl[row + 2];
   const double rinv = G.rinv, r = G.r;
-#if SPH_D2_QH
   const double sv = G.q; // q
-#else
-  const double sv = fma(-r, I.inv_h, t3.x); // c_off - q
-#endif
   const double b3 = fma(t1.x, sv, t1.y), b2 = fma(b3, sv, t2.x), b1 = fma(b2, sv, t2.y);
   const double P = fma(b1, sv, t3.y);
   const double D = fma(fma(fma(t1.x, sv, b3), sv, b2), sv, b1); // P'(s) = 4 E
@@ -1017,11 +999,7 @@ __device__ __forceinline__ void density2_item(const DenArgs &A, D2Tile (&tiles)[
     }
   }
   if (!live || qs != 0) return;
-#if SPH_D2_QH
   constexpr double kDs = -0.25; // accumulated with dP/dq = -4 E
-#else
-  constexpr double kDs = 0.25; // accumulated with dP/ds = 4 E
-#endif
   s.qe *= kDs * I.inv_h; // accumulated as sum r (4 m E): to sum q m E
   s.div *= kDs;
   s.rot *= kDs;
