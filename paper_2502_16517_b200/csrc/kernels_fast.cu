@@ -920,7 +920,7 @@ __device__ __forceinline__ void density2_item(const DenArgs &A, D2Tile (&tiles)[
       // into tiles_w[2], padded with inert dummies to the pair loop's granule
       int nj = kTJ;
       const D2Tile *Tp = &tiles_w[buf];
-      if constexpr (JS == 1) { // (rounds >= 1 with j-slices: measured slower)
+      if constexpr (JS == 1) { // (for j-slice warps measured slower: round 1 +8 %)
         constexpr int PADQ = JS * ((kTJ / JS) < 4 ? (kTJ / JS) : 4); // pair-loop granule
         const D2Tile &S = tiles_w[buf];
         D2Tile &C = tiles_w[2];
