@@ -414,7 +414,8 @@ constexpr int kF2W = SPH_F2_WPC, kD2W = SPH_D2_WPC;
 #endif
 constexpr int kF2FarU = SPH_F2_FARU;
 #ifndef SPH_F2_NEARU
-#define SPH_F2_NEARU 4 // near loop unroll (pairs of pairs; measured 2: -0.9 %, 4: -1.9 %, 8: +1.5 %)
+#define SPH_F2_NEARU 8 // near loop unroll (pairs of pairs; r1: 2 -0.9 %, 4 -1.9 % vs 1; r2 with the
+                       // persistent q-form kernel: 8 -0.7 % vs 4, 16 +19 %, profiles/r2u_unroll.txt)
 #endif
 constexpr int kF2NearU = SPH_F2_NEARU;
 #ifndef SPH_D2_U
