@@ -169,6 +169,9 @@ int sph_make_particles_ex(sph_ctx *ctx, int64_t n, int ppc, uint64_t seed, int k
  * order for sph_make_particles contexts). */
 int sph_read_records(sph_ctx *ctx, void *out_records);
 
+/* Counters and timings of the last sweeps / step. Counts that are still in flight to the host
+ * (the work list built by the last rebin) are waited for, so this may synchronise the
+ * context's stream. */
 int sph_get_stats(const sph_ctx *ctx, sph_stats *out);
 int sph_synchronize(sph_ctx *ctx);
 
