@@ -195,10 +195,11 @@ struct sph_ctx {
   // pipelined end-to-end step (sph_step_host): force chunks on two streams, per-chunk
   // kick2 + host-order compaction on `post`, device->host copies on `copy`
   cudaStream_t fs[2]{}, post = nullptr, copy = nullptr;
-  cudaEvent_t pev[40]{};
+  cudaEvent_t pev[72]{};
   int pipeline = 1; // env SPH_B200_PIPELINE=0: serial force -> kick2 -> download
-  static constexpr int kMaxPipeK = 16;
-  int pipe_k = 16;  // env SPH_B200_PIPE_K: force chunks of the pipelined step (2..16); 16 vs 8: exposed tail 1.57 -> 1.04 ms
+  static constexpr int kMaxPipeK = 32;
+  int pipe_k = 16;  // env SPH_B200_PIPE_K: force chunks of the pipelined step (2..32); 16 vs 8: exposed tail 1.57 -> 1.04 ms
+  int pipe_tail = 2; // env SPH_B200_PIPE_TAIL: shrinking last chunks (2: the last two half size)
   std::string err;
   int numerics = SPH_NUMERICS_FAST;
   int layout = SPH_LAYOUT_FROM_PATH;
@@ -840,16 +841,25 @@ struct sph_ctx {
     B.k = K;
     int kb[kMaxPipeK + 1];
     {
+      // the last T chunks shrink (1/2, 1/4, ... of a full one, the last two equal): the last
+      // chunk's records are the exposed copy (T = 2: the last two half size)
+      const int T = std::max(1, std::min(pipe_tail, K - 1));
+      double w[kMaxPipeK];
+      double tot = 0.0;
+      for (int f = 0; f < K; ++f) {
+        const int t = f - (K - T); // 0 .. T-1 in the tail
+        w[f] = (t < 0 || T == 1) ? 1.0 : std::ldexp(1.0, -(std::min(t, T - 2) + 1));
+        tot += w[f];
+      }
       int c = 0;
-      // the last two chunks are half size: the last chunk's records are the exposed copy
-      const double unit = 1.0 / (K - 1);
+      double acc = 0.0;
       for (int f = 0; f <= K; ++f) {
-        const double frac = std::min(f, K - 2) * unit + std::max(0, f - (K - 2)) * 0.5 * unit;
-        const long long target = (long long)std::llround((double)n * frac);
+        const long long target = (long long)std::llround((double)n * acc / tot);
         while (c < ncells && cb[c] < target) ++c;
         if (f == K) c = ncells;
         B.s[f] = cb[c];
         kb[f] = kpre[c];
+        if (f < K) acc += w[f];
       }
     }
     // host chunk -> last force chunk
@@ -1599,6 +1609,7 @@ int sph_create(int device, sph_ctx **out) {
   if (const char *e = std::getenv("SPH_B200_PIPELINE")) ctx->pipeline = std::atoi(e);
   if (const char *e = std::getenv("SPH_B200_PIPE_K"))
     ctx->pipe_k = std::min(sph_ctx::kMaxPipeK, std::max(2, std::atoi(e)));
+  if (const char *e = std::getenv("SPH_B200_PIPE_TAIL")) ctx->pipe_tail = std::max(1, std::atoi(e));
   if (const char *e = std::getenv("SPH_B200_DEN_JS0")) ctx->den_js0 = std::atoi(e);
   if (const char *e = std::getenv("SPH_B200_DEN_JS1")) ctx->den_js1 = std::atoi(e);
   if (const char *e = std::getenv("SPH_B200_DEN_DENSE")) ctx->den_dense_frac = std::atof(e);

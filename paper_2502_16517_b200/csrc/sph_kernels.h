@@ -55,7 +55,7 @@ void launch_scatter_idx(double *dst, const double *src, const int *idx, int m, c
 // slot ranges of the pipelined force chunks; dep[g] = last chunk touching host chunk g
 struct ChunkBounds {
   int k;      // chunks
-  int s[17];  // slot bounds, s[0] = 0, s[k] = n
+  int s[33];  // slot bounds, s[0] = 0, s[k] = n (k <= 32)
 };
 void launch_host_chunk_dep(int *dep, const int *host_idx, int n, int hsz, const ChunkBounds &b,
                            cudaStream_t s);
