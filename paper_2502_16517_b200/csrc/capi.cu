@@ -557,7 +557,6 @@ struct sph_ctx {
     int nitems = n_items0;
     items_a.ensure((size_t)ncells + (size_t)n / (kTI / std::max(js0, js1)) + 1);
     items_b.ensure((size_t)ncells + (size_t)n / (kTI / std::max(js0, js1)) + 1);
-    int js_next = js1; // lanes per particle of the next round (adaptive, see below)
     if (js0 > 1) { // round-0 items of 32/js0 particles
       launch_make_items(items_b.p, scalars.p, pairs_dev.p, cnt.p, cell_begin.p, na_cell.p,
                         cell_order.p, ncells, stream, kTI / js0, items_scratch());
