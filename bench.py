@@ -324,12 +324,13 @@ def run_decomposed(args, rank, world, local):
     }
     # e2e: the rank's owned records come from pinned host memory before every step and go
     # back after it (sph_dd_append / sph_dd_export through the C-ABI)
-    if args.e2e_steps > 0:
+    e2e_steps = args.steps if args.e2e_steps is None else args.e2e_steps
+    if e2e_steps > 0:
         allm = np.ones(nx, np.uint8)
         host = torch.empty(n_local * 272 + 4096, dtype=torch.uint8, pin_memory=True)
         hrank = torch.empty(n_local + 16, dtype=torch.int64, pin_memory=True)
         wall = []
-        for it in range(args.e2e_steps + 1):
+        for it in range(e2e_steps + 1):
             dist.barrier()
             t1 = time.perf_counter()
             if it > 0:  # host -> device: replace the device state with the host records
@@ -354,7 +355,7 @@ def run_decomposed(args, rank, world, local):
         nb = total(n_local * 272, dist.ReduceOp.MAX)
         out["e2e"] = {"value": workload_pairs / e2e_s, "unit": UNIT,
                       "h2d_bytes_per_step": int(nb), "d2h_bytes_per_step": int(nb),
-                      "ms_per_step": e2e_s * 1e3, "steps": args.e2e_steps,
+                      "ms_per_step": e2e_s * 1e3, "steps": e2e_steps,
                       "api": "per rank: H2D of the owned records (sph_dd_append), the "
                              "decomposed step, D2H of the owned records (sph_dd_export)"}
     ctx.close()
@@ -427,13 +428,18 @@ def run_single(args, rank, world, local):
     }
 
     # ---- e2e: the same step through the C-ABI on pinned host records ----
-    e2e_steps = args.e2e_steps
+    e2e_steps = args.steps if args.e2e_steps is None else args.e2e_steps
     if e2e_steps <= 0:
         return _finish(out, ctx, store, grid, par, args, rank, world, ph, names, den_eval,
                        workload_pairs)
+    # the host records still hold the initial condition: the end-to-end run repeats the
+    # device run's trajectory, W warm-up steps then the timed ones (steps W+1 .. W+E), so
+    # `value`, `e2e` and the reference arm all time the same simulated steps (the density work
+    # grows with simulated time)
     ctx.host_register(store.recs)
     try:
-        ctx.step_host(par)  # warm-up
+        for _ in range(args.warmup):
+            ctx.step_host(par)
         barrier(world)
         wall = []
         dev = np.zeros(8)
@@ -450,6 +456,10 @@ def run_single(args, rank, world, local):
                   "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": nbytes,
                   "ms_per_step": e2e_s * 1e3, "steps": e2e_steps,
                   "api": "sph_step_host (C-ABI, host Particle records in and out)",
+                  "trajectory": (f"from the initial condition, {args.warmup} warm-up steps, "
+                                 f"timed steps {args.warmup + 1}-{args.warmup + e2e_steps} "
+                                 f"(the device run times steps {args.warmup + 1}-"
+                                 f"{args.warmup + args.steps})"),
                   "device_ms": dict(zip(["h2d"] + names + ["d2h"],
                                         (dev / e2e_steps).round(3).tolist()))}
     return _finish(out, ctx, store, grid, par, args, rank, world, ph, names, den_eval,
@@ -624,7 +634,9 @@ def main():
     ap.add_argument("--numerics", default="fast", choices=["fast", "exact"])
     ap.add_argument("--ic", default="uniform", choices=["uniform", "clustered"])
     ap.add_argument("--layout", default="resident", choices=["resident", "aos", "convert"])
-    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--e2e-steps", type=int, default=None,
+                    help="timed end-to-end steps (default: --steps, after --warmup warm-up "
+                         "steps from the initial condition: the device run's trajectory)")
     ap.add_argument("--strong", action="store_true",
                     help="N > 1: --particles is the global box (BASELINE config 5 strong scaling) "
                          "instead of the per-GPU count (weak scaling, the default)")
