@@ -392,14 +392,19 @@ def run_single(args, rank, world, local):
     den_eval = 0
     round_ms = np.zeros(4)
     steps_ms = []
+    mid_state = None  # the CPU baseline times the middle step of the timed range
     with ClockSampler(local) as clk:
-        for _ in range(args.steps):
+        for it in range(args.steps):
+            if it == args.steps // 2 and world == 1 and args.cpu_baseline:
+                mid_state = ctx.read_records()  # between steps: outside the device-event time
             ms = ctx.step(par)
             st = ctx.stats()
             den_eval += st["density_pairs"]
             round_ms += np.array(st["density_round_ms"])
             phase += ms
             steps_ms.append(float(ms.sum()))
+    args.mid_state = mid_state
+    args.mid_step = args.warmup + args.steps // 2 + 1
     ctx.synchronize()
     launches = ctx.launch_count() - launches0
     barrier(world)
@@ -538,11 +543,14 @@ def _host_state(ctx, store):
 
 
 def cpu_baseline(ctx, store, grid, par, args):
-    """One full reference step (oracle/_ref) from the device's current state, on all host
-    cores, wall clock; rank 0 at N = 1 only."""
+    """One full reference step (oracle/_ref) of the middle step of the timed range (the state
+    the device run had there; the density work grows with simulated time), on all host cores,
+    wall clock; rank 0 at N = 1 only."""
     from oracle.ref_bench import ReferenceStepper
-    st = _host_state(ctx, store)
-    stepper = ReferenceStepper(st.recs, args.ppc, par.as_array(), sample_pairs=args.cpu_sample_pairs)
+    recs = getattr(args, "mid_state", None)
+    if recs is None:
+        recs = _host_state(ctx, store).recs
+    stepper = ReferenceStepper(recs, args.ppc, par.as_array(), sample_pairs=args.cpu_sample_pairs)
     t = stepper.step()
     frac = t["sample_fraction"]
     what = ("density and force on every cell" if frac >= 1.0 else
@@ -552,8 +560,9 @@ def cpu_baseline(ctx, store, grid, par, args):
             "cores": stepper.threads, "kind": "reference",
             "step_seconds": t["step"], "measured_seconds": t["measured_seconds"],
             "sample": f"one full reference step (kick1, drift, build_grid, kick2 on all {args.n} "
-                      f"particles; {what}) of the same workload state; oracle/_ref built from "
-                      f"/root/reference; wall clock",
+                      f"particles; {what}) of the same workload: simulated step "
+                      f"{getattr(args, 'mid_step', '?')}, the middle of the timed range; "
+                      f"oracle/_ref built from /root/reference; wall clock",
             "phase_seconds": {k: round(t[k], 4) for k in
                               ("kick1", "drift", "rebin", "density", "force", "kick2")}}
 
