@@ -238,6 +238,10 @@ struct sph_ctx {
   DevBuf<long long> all_rank, all_rank_tmp, pairs_dev, pairs_dev2; // {sum nl*na, particles}
   DevBuf<unsigned long long> fail_dev; // density: particles that hit the 30-round limit
   DevBuf<int> item_ctr;                 // density: persistent-round item counters
+  // resident mirror: the AoS record fields without a SoA array (id, cell, dbg[1], spare) of
+  // slot k live at aos[home[k]] while home_on (the fix-up rebin moves the map, not them)
+  DevBuf<int> home, home_tmp;
+  bool home_on = false;
   DevBuf<int> f2_ctr;                   // force2 persistent launches: item counters (per stream)
   DevBuf<unsigned long long> keys, keys_sorted;
   DevBuf<unsigned> cost_key, cost_key_sorted;
@@ -336,7 +340,7 @@ struct sph_ctx {
     cub_tmp.release(); h_stage.release(); h_small.release(); owned.release();
     items0_n.release(); pairs0_dev.release(); h_items0.release();
     items_c.release(); items_d2.release(); cnt_sp.release(); cnt_dn.release(); pairs_dev2.release();
-    item_ctr.release(); f2_ctr.release();
+    item_ctr.release(); f2_ctr.release(); home.release(); home_tmp.release();
     items_g.release(); hdep.release(); sub_mask.release(); sub_cnt.release(); items_sub.release();
     dd_mask.release(); dd_flag.release(); dd_sel.release(); dd_cnt.release();
     mi_k.release(); mi_off.release(); mi_tmp.release();
@@ -490,7 +494,18 @@ struct sph_ctx {
   }
 
   // ---- mirror coherence ----
+  // the record tails back into slot order (aos[k] holds slot k's id, cell, dbg[1], spare)
+  void normalize_tails() {
+    if (!home_on) return;
+    aos_tmp.ensure(n);
+    launch_permute_record_tails(aos_tmp.p, aos.p, home.p, (int)n, stream);
+    launched();
+    std::swap(aos.p, aos_tmp.p);
+    std::swap(aos.cap, aos_tmp.cap);
+    home_on = false;
+  }
   void make_aos_current() {
+    normalize_tails();
     if (soa_ahead) {
       launch_scatter(aos.p, soa, (int)n, kSoaFields, stream);
       launched();
@@ -500,6 +515,7 @@ struct sph_ctx {
   void make_soa_current() {
     ensure_soa();
     if (!soa_valid) {
+      normalize_tails();
       launch_gather(aos.p, soa, (int)n, kSoaFields, stream);
       launched();
       soa_valid = true;
@@ -904,7 +920,7 @@ struct sph_ctx {
       if (s1 > s0) {
         SoaMirror o = soa_at(s0);
         launch_linear(SPH_KICK2, false, aos.p + s0, o, s1 - s0, par, post);
-        launch_compact_soa(dn, aos.p, soa, host_idx.p, s0, s1, post);
+        launch_compact_soa(dn, aos.p, soa, host_idx.p, home_on ? home.p : nullptr, s0, s1, post);
         launched(2);
       }
       CK(cudaEventRecord(pev[1 + K + f], post)); // slots of chunk f final in `dense`
@@ -980,6 +996,7 @@ struct sph_ctx {
   }
   int64_t dd_export(const uint8_t *col_mask, Particle *out, long long *ranks_out, int64_t cap) {
     if (n == 0) return 0;
+    normalize_tails();
     const int64_t m = dd_select(col_mask, false);
     if (m > cap) throw ArgError{"export buffer too small"};
     if (soa_ahead) // resident: assemble the selected records from the SoA mirror + tails
@@ -999,6 +1016,7 @@ struct sph_ctx {
   }
   void dd_remove(const uint8_t *col_mask) {
     if (n == 0) return;
+    normalize_tails();
     const int64_t keep = dd_select(col_mask, true);
     if (keep == n) return;
     apply_perm(dd_sel.p, keep); // (sel is read before the buffers it indexes are swapped)
@@ -1010,6 +1028,7 @@ struct sph_ctx {
   }
   void dd_append(const Particle *recs, const long long *ranks, int64_t m) {
     if (m <= 0) return;
+    normalize_tails();
     if (n + m >= (1LL << 31)) throw ArgError{"particle count out of range"};
     if (soa_ahead || soa_valid) {
       // resident: the records go to the AoS mirror and their fields straight into the SoA
@@ -1094,6 +1113,7 @@ struct sph_ctx {
   // Halo particles appended from their payload: SoA fields (the rest zero), zero record tails.
   void dd_append_halo(const double *in, const long long *ranks, int64_t m) {
     if (m <= 0) return;
+    normalize_tails();
     if (n + m >= (1LL << 31)) throw ArgError{"particle count out of range"};
     make_soa_current();
     soa_ahead = true; // the appended particles exist in the SoA mirror only
@@ -1216,6 +1236,7 @@ struct sph_ctx {
     }
     soa_valid = false;
     soa_ahead = false;
+    home_on = false; // whole records, slot order
     dirty = 0;
     return true;
   }
@@ -1249,6 +1270,7 @@ struct sph_ctx {
     }
     soa_valid = false;
     soa_ahead = false;
+    home_on = false; // whole records, slot order
     dirty = 0;
   }
 
@@ -1357,6 +1379,7 @@ struct sph_ctx {
   // smaller than n: the dropped slots vanish). AoS, host_idx, all_rank, and the SoA arrays
   // when they hold data.
   void apply_perm(const int *perm, int64_t m) {
+    normalize_tails();
     aos_tmp.ensure(m);
     if (soa_ahead) // the SoA is the truth: move only the AoS-only fields
       launch_permute_record_tails(aos_tmp.p, aos.p, perm, (int)m, stream);
@@ -1451,19 +1474,29 @@ struct sph_ctx {
     }
     host_idx_tmp.ensure(n);
     all_rank_tmp.ensure(n);
-    aos_tmp.ensure(n);
-    // resident (SoA ahead): only the record fields without a SoA array move with the SoA;
-    // otherwise whole records, then p->cell
+    auto sw = [](auto &a, auto &b) { std::swap(a.p, b.p); std::swap(a.cap, b.cap); };
+    // resident (SoA ahead): the record fields without a SoA array stay in place and the
+    // slot -> record map moves instead (a mover's p->cell written where it lives);
+    // otherwise whole records move, then p->cell
+    if (soa_ahead) {
+      home.ensure(n);
+      home_tmp.ensure(n);
+    }
     launch_permute_fused(fx_perm.p, N, soa, dst, soa_data, host_idx.p, host_idx_tmp.p,
-                         all_rank.p, all_rank_tmp.p, cellnew.p, slot_cell_tmp.p, aos.p,
-                         soa_ahead ? aos_tmp.p : nullptr, in_step, stream);
+                         all_rank.p, all_rank_tmp.p, cellnew.p, slot_cell_tmp.p, slot_cell.p,
+                         soa_ahead && home_on ? home.p : nullptr,
+                         soa_ahead ? home_tmp.p : nullptr, aos.p, in_step, stream);
     launched();
-    if (!soa_ahead) {
+    if (soa_ahead) {
+      sw(home, home_tmp);
+      home_on = true;
+    } else {
+      aos_tmp.ensure(n);
       launch_permute<Particle>(aos_tmp.p, aos.p, fx_perm.p, N, stream);
       launched();
+      sw(aos, aos_tmp);
     }
-    auto sw = [](auto &a, auto &b) { std::swap(a.p, b.p); std::swap(a.cap, b.cap); };
-    sw(aos, aos_tmp); sw(host_idx, host_idx_tmp); sw(all_rank, all_rank_tmp);
+    sw(host_idx, host_idx_tmp); sw(all_rank, all_rank_tmp);
     sw(slot_cell, slot_cell_tmp); sw(cell_begin, fx_new_begin);
     if (soa_data) {
       sw(f_x, g_x); sw(f_v, g_v); sw(f_vp, g_vp); sw(f_a, g_a); sw(f_m, g_m); sw(f_rho, g_rho);

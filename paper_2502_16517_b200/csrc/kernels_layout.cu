@@ -121,8 +121,8 @@ __global__ void compact_kernel(uint4 *__restrict__ dense, const uint4 *__restric
 // record. One thread per 16-byte piece k of a record; the piece layout follows
 // particle.hpp:11-46 (k = offset / 16).
 __global__ void compact_soa_kernel(uint4 *__restrict__ dense, const uint4 *__restrict__ aos,
-                                   SoaMirror f, const int *__restrict__ host_idx, int s0,
-                                   long long total) {
+                                   SoaMirror f, const int *__restrict__ host_idx,
+                                   const int *__restrict__ home, int s0, long long total) {
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
        i += (long long)gridDim.x * blockDim.x) {
     const long long r = i / 17;
@@ -156,7 +156,7 @@ __global__ void compact_soa_kernel(uint4 *__restrict__ dense, const uint4 *__res
                      __double2loint(d), __double2hiint(d));
       break;
     }
-    default: v = aos[(long long)s * 17 + k]; break; // id/cell, dbg[1], spare
+    default: v = aos[(long long)(home ? home[s] : s) * 17 + k]; break; // id/cell, dbg[1], spare
     }
     dense[(long long)host_idx[s] * 17 + k] = v;
   }
@@ -578,13 +578,14 @@ __global__ void fixup_newslot_kernel(int *__restrict__ perm, const int *__restri
 // where density then force rewrite a, rho, u_dt, wcount, rho_dh, rot_v, div_v, v_sig of
 // every particle before any kernel reads them (kernels.cpp:194-202, :369-376), so those
 // eight arrays are not moved.
-template <bool SOA, bool TAILS>
+template <bool SOA, bool HOME>
 __global__ void permute_fused_kernel(const int *__restrict__ perm, int n, SoaMirror src,
                                      SoaMirror dst, const int *__restrict__ hid_src,
                                      int *__restrict__ hid_dst, const long long *__restrict__ ar_src,
                                      long long *__restrict__ ar_dst, const int *__restrict__ cellnew,
-                                     int *__restrict__ slot_cell, const Particle *__restrict__ rsrc,
-                                     Particle *__restrict__ rdst, bool step_dead) {
+                                     int *__restrict__ slot_cell, const int *__restrict__ cell_old,
+                                     const int *__restrict__ home_src, int *__restrict__ home_dst,
+                                     Particle *__restrict__ aos, bool step_dead) {
   const int k = blockIdx.x * blockDim.x + threadIdx.x;
   if (k >= n) return;
   const int s = perm[k];
@@ -604,17 +605,12 @@ __global__ void permute_fused_kernel(const int *__restrict__ perm, int n, SoaMir
       dst.div_v[k] = src.div_v[s]; dst.v_sig[k] = src.v_sig[s];
     }
   }
-  if (TAILS) {
-    const uint4 *a = reinterpret_cast<const uint4 *>(rsrc + s);
-    uint4 *b = reinterpret_cast<uint4 *>(rdst + k);
-    uint4 t = a[12]; // id (192), cell (200)
-    const long long cl = c;
-    t.z = (unsigned)cl;
-    t.w = (unsigned)(cl >> 32);
-    b[12] = t;
-    b[14] = a[14]; // dbg[1] (224), spare[0] (232)
-    b[15] = a[15];
-    b[16] = a[16];
+  if (HOME) {
+    // the record fields without a SoA array (id, cell, dbg[1], spare) stay where they are:
+    // slot k's live at aos[home[k]]; only a mover's p->cell changes (grid.cpp:156)
+    const int h = home_src ? home_src[s] : s;
+    home_dst[k] = h;
+    if (c != cell_old[s]) aos[h].cell = c;
   }
 }
 
@@ -800,12 +796,12 @@ void launch_scatter_idx(double *dst, const double *src, const int *idx, int m, c
 }
 
 void launch_compact_soa(Particle *dense, const Particle *aos, const SoaMirror &f,
-                        const int *host_idx, int s0, int s1, cudaStream_t s) {
+                        const int *host_idx, const int *home, int s0, int s1, cudaStream_t s) {
   const long long total = 17LL * (s1 - s0);
   if (total > 0)
     compact_soa_kernel<<<grid_for(total, 256), 256, 0, s>>>(reinterpret_cast<uint4 *>(dense),
                                                              reinterpret_cast<const uint4 *>(aos),
-                                                             f, host_idx, s0, total);
+                                                             f, host_idx, home, s0, total);
 }
 void launch_host_chunk_dep(int *dep, const int *host_idx, int n, int hsz, const ChunkBounds &b,
                            cudaStream_t s) {
@@ -986,17 +982,16 @@ void launch_rebin_fixup(const FixupArgs &a, cudaStream_t s) {
 void launch_permute_fused(const int *perm, int n, const SoaMirror &src, const SoaMirror &dst,
                           bool soa, const int *hid_src, int *hid_dst, const long long *ar_src,
                           long long *ar_dst, const int *cellnew, int *slot_cell,
-                          const Particle *rsrc, Particle *rdst, bool step_dead, cudaStream_t s) {
+                          const int *cell_old, const int *home_src, int *home_dst, Particle *aos,
+                          bool step_dead, cudaStream_t s) {
   if (n <= 0) return;
   const int g = (n + 255) / 256;
-  if (soa && rdst)
-    permute_fused_kernel<true, true><<<g, 256, 0, s>>>(perm, n, src, dst, hid_src, hid_dst, ar_src, ar_dst, cellnew, slot_cell, rsrc, rdst, step_dead);
+  if (soa && home_dst)
+    permute_fused_kernel<true, true><<<g, 256, 0, s>>>(perm, n, src, dst, hid_src, hid_dst, ar_src, ar_dst, cellnew, slot_cell, cell_old, home_src, home_dst, aos, step_dead);
   else if (soa)
-    permute_fused_kernel<true, false><<<g, 256, 0, s>>>(perm, n, src, dst, hid_src, hid_dst, ar_src, ar_dst, cellnew, slot_cell, rsrc, rdst, step_dead);
-  else if (rdst)
-    permute_fused_kernel<false, true><<<g, 256, 0, s>>>(perm, n, src, dst, hid_src, hid_dst, ar_src, ar_dst, cellnew, slot_cell, rsrc, rdst, step_dead);
+    permute_fused_kernel<true, false><<<g, 256, 0, s>>>(perm, n, src, dst, hid_src, hid_dst, ar_src, ar_dst, cellnew, slot_cell, cell_old, home_src, home_dst, aos, step_dead);
   else
-    permute_fused_kernel<false, false><<<g, 256, 0, s>>>(perm, n, src, dst, hid_src, hid_dst, ar_src, ar_dst, cellnew, slot_cell, rsrc, rdst, step_dead);
+    permute_fused_kernel<false, false><<<g, 256, 0, s>>>(perm, n, src, dst, hid_src, hid_dst, ar_src, ar_dst, cellnew, slot_cell, cell_old, home_src, home_dst, aos, step_dead);
 }
 void launch_slot_cell_from_keys(int *slot_cell, const unsigned long long *keys, int n,
                                 cudaStream_t s) {

@@ -44,9 +44,9 @@ void launch_scatter(Particle *aos, const SoaMirror &f, int n, uint32_t mask, cud
 void launch_expand(Particle *aos, const Particle *dense, const int *host_idx, int n, cudaStream_t s);
 void launch_compact(Particle *dense, const Particle *aos, const int *host_idx, int n, cudaStream_t s);
 // host-order records of slots [s0, s1) assembled from the resident SoA (+ AoS for the
-// fields without a SoA array)
+// fields without a SoA array, at aos[home[slot]] when home is set)
 void launch_compact_soa(Particle *dense, const Particle *aos, const SoaMirror &f,
-                        const int *host_idx, int s0, int s1, cudaStream_t s);
+                        const int *host_idx, const int *home, int s0, int s1, cudaStream_t s);
 // domain decomposition: column-mask flags per slot, iota, indexed scatter
 void launch_col_flags(unsigned char *flag, const Particle *aos, const SoaMirror &f, bool aos_src,
                       const unsigned char *mask, int n, int nx, int invert, cudaStream_t s);
@@ -124,10 +124,15 @@ size_t fixup_scan_bytes(int n);
 void launch_rebin_fixup(const FixupArgs &a, cudaStream_t s);
 // dst[k] = src[perm[k]] for the SoA mirror (soa), host_idx, all_rank, slot_cell := cellnew[perm]
 // and, with rdst, the record tails (id, cell := new cell, dbg[1], spare)
+// fused fix-up permute: slot k <- old slot perm[k] for the per-slot arrays (and the SoA
+// mirror when `soa`); with home_dst set (resident mirror) the AoS record tails stay in place
+// and home_dst[k] records where slot k's tail lives (home_src: the previous map, or null for
+// identity), a mover's p->cell written there
 void launch_permute_fused(const int *perm, int n, const SoaMirror &src, const SoaMirror &dst,
                           bool soa, const int *hid_src, int *hid_dst, const long long *ar_src,
                           long long *ar_dst, const int *cellnew, int *slot_cell,
-                          const Particle *rsrc, Particle *rdst, bool step_dead, cudaStream_t s);
+                          const int *cell_old, const int *home_src, int *home_dst, Particle *aos,
+                          bool step_dead, cudaStream_t s);
 void launch_slot_cell_from_keys(int *slot_cell, const unsigned long long *keys, int n,
                                 cudaStream_t s);
 // device-resident decomposition: records of the selected slots from the SoA mirror + record
