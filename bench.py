@@ -494,6 +494,9 @@ def _finish(out, ctx, store, grid, par, args, rank, world, ph, names, den_eval, 
             "note": "force evaluates gravity on every active pair (nothing culled), so this "
                     "is bounded by the FP64 pipe",
         }
+        pipe_f = load_pipe("force2_kernel")
+        if pipe_f is not None:  # the hardware view beside the algorithmic-flop one
+            out["roofline"]["fp64_pipe_pct_ncu"] = pipe_f
         cull_note = ("effective: the reference's algorithmic flops for every active pair "
                      "(SURVEY 8(d)); density skips chunks out of the warp's reach, so on "
                      "clustered boxes this can exceed the pipe peak; not pipe utilisation")
