@@ -355,3 +355,47 @@ def test_sweep_scheduling_does_not_change_results(monkeypatch, kind):
             rounds.append(r)
     assert rounds[0] >= 2 and rounds[0] == rounds[1], rounds
     assert outs[0] == outs[1]
+
+
+def test_record_tails_follow_the_slots_across_layout_switches(orc):
+    """Resident steps with particles crossing cells leave the record fields without a SoA
+    array (id, cell, dbg[1], spare) in place and move a slot -> record map instead; a switch
+    to the AoS layout, an AoS sweep, more resident steps and a full read-back must still
+    give the oracle's records byte for byte (EXACT numerics; the spare words carry a
+    per-particle marker so a misplaced tail cannot go unnoticed)."""
+    n, ppc, seed = 6000, 64, 8
+    recs0, par = orc.make_particles(n, ppc, seed)
+    recs0["spare"][:, 0] = np.arange(n, dtype=np.float64) * 0.5 + 1.0  # untouched by every kernel
+    recs0["dbg"][:, 1] = -np.arange(n, dtype=np.float64)
+    par = SphParams(dt=2e-3, gamma=par.gamma, cfl=par.cfl, grav=par.grav,
+                    target_wcount=par.target_wcount)
+    recs = recs0.copy()
+    store = pkg.ParticleStore(recs, np.arange(n, dtype=np.int64), pkg.Layout.Continuous)
+    grid = pkg.build_grid(store, pkg.InitConfig(n=n, ppc=ppc))
+    ref = recs0.copy()
+    nx = grid.nx
+
+    def oracle_step():
+        for k in (KernelId.Kick1, KernelId.Drift):
+            cb, li = orc.build_grid(ref, nx)
+            orc.sweep(int(k), ref, nx, nx, 1.0 / nx, cb, li, par)
+        cb, li = orc.build_grid(ref, nx)
+        for k in (KernelId.Density, KernelId.Force, KernelId.Kick2):
+            orc.sweep(int(k), ref, nx, nx, 1.0 / nx, cb, li, par)
+
+    with pkg.Context(0, numerics=Numerics.Exact, layout=DeviceLayout.Resident) as ctx:
+        ctx.bind(grid)
+        for _ in range(2):
+            ctx.step(par)
+            oracle_step()
+        ctx.set_layout(DeviceLayout.Aos)  # the AoS copy becomes the truth: tails back in place
+        ctx.sweep(KernelId.Kick1, par)
+        cb, li = orc.build_grid(ref, nx)
+        orc.sweep(int(KernelId.Kick1), ref, nx, nx, 1.0 / nx, cb, li, par)
+        ctx.set_layout(DeviceLayout.Resident)
+        for _ in range(2):
+            ctx.step(par)
+            oracle_step()
+        got = ctx.read_records()
+    assert np.count_nonzero(ref["cell"] != recs0["cell"]) > 0, "particles must change cells"
+    assert got.tobytes() == ref.tobytes()
