@@ -122,7 +122,12 @@ def _median(v):
 def run_bench(cfg: BenchConfig, ctx: Context | None = None) -> list[BenchRecord]:
     """bench.cpp:135-217 on the device: per ppc, one IC per store layout (the reference IC
     from sph_make_particles), one warm-up sweep, `reps` timed sweeps from the restored IC,
-    medians; soa-view records are cross-checked against the exact device sweep."""
+    medians; soa-view records are cross-checked against the exact device sweep. (The
+    reference's cross_compare runs the CPU path; product code here may not call the
+    test-only oracle, so this mirror compares with the EXACT device sweep, which the GPU
+    tests pin byte for byte to the reference. The reference's own run_bench, cross-checking
+    against its CPU rows, runs on the B200 through the link-time drop-in: INTEGRATION.md
+    §2b, profiles/r2_reference_bench_harness_gpu.csv.)"""
     out: list[BenchRecord] = []
     if cfg.reps <= 0:
         return out
