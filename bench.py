@@ -43,7 +43,6 @@ sys.path.insert(0, ROOT)
 
 METRIC = "particle-pair interactions/sec (density+force)"
 UNIT = "pairs/s"
-F_IN_REF = (0.2236, 0.0804, 0.0089)  # SURVEY.md §8(d), reference IC at ppc 1024
 IC_KIND = {"uniform": 0, "clustered": 1}  # clustered = BASELINE config 3 (sph_b200.h)
 
 
@@ -186,42 +185,6 @@ def allmax(v, world):
     t = torch.tensor([v], dtype=torch.float64, device="cuda")
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
-
-
-def pair_fractions(store, grid, ncells_sample=64, seed=1, pairs_per_cell=2e8):
-    """In-support fractions of the current state, pair-weighted: cells are drawn with
-    probability proportional to their pair count nl * na (so the dense cells of a clustered
-    box, which hold most of the pairs, are represented) and the per-cell fractions averaged
-    (unbiased for the pair-weighted mean). Oracle statistics on host records."""
-    from oracle import Oracle
-    orc = Oracle()
-    rng = np.random.default_rng(seed)
-    cb = np.asarray(grid.cell_begin, np.int64)
-    nl = np.diff(cb).astype(np.float64)
-    nx, ny = grid.nx, grid.ny
-    na = np.zeros_like(nl)
-    cy, cx = np.divmod(np.arange(nx * ny), nx)
-    seen = set()
-    for dy in (-1, 0, 1):
-        for dx in (-1, 0, 1):
-            if (dy % ny, dx % nx) in seen:
-                continue
-            seen.add((dy % ny, dx % nx))
-            na += nl[((cy + dy) % ny) * nx + (cx + dx) % nx]
-    w = nl * na
-    if w.sum() <= 0:
-        return F_IN_REF
-    cells = rng.choice(nx * ny, size=ncells_sample, replace=True, p=w / w.sum())
-    fr = []
-    for c in np.unique(cells):
-        # every stride-th local of the cell: <= ~2e8 pairs per sampled cell (the dense cells
-        # of a clustered 2^24 box hold ~1e10)
-        stride = max(1, int(np.ceil(w[c] / pairs_per_cell)))
-        st = orc.pair_stats_cell(store.recs, nx, ny, grid.cell_begin, grid.local_idx, c, stride)
-        if st[0]:
-            fr.append((np.count_nonzero(cells == c), st[2] / st[0], st[3] / st[0], st[4] / st[0]))
-    k = np.array([f[0] for f in fr], np.float64)
-    return tuple(float(np.dot(k, [f[i] for f in fr]) / k.sum()) for i in (1, 2, 3))
 
 
 def config_block(args, nx, world):
@@ -475,10 +438,9 @@ def _finish(out, ctx, store, grid, par, args, rank, world, ph, names, den_eval, 
     if rank == 0:
         fp64 = ctx.fp64_peak_tflops()
         peaks, src = load_peaks()
-        try:
-            fin, f15, f05 = pair_fractions(_host_state(ctx, store), grid)
-        except Exception:
-            fin, f15, f05 = F_IN_REF
+        # exact support fractions of the final state: a device counting pass with the
+        # reference's arithmetic, outside the timed region (sph_pair_fractions)
+        fin, f15, f05, _ = ctx.pair_fractions()
         dfl, ffl = flops_per_pair(fin, f15, f05)
         fpairs = workload_pairs / 2
         ach_f = ffl * fpairs / (ph[4] * 1e-3) / 1e12
@@ -531,7 +493,9 @@ def _finish(out, ctx, store, grid, par, args, rank, world, ph, names, den_eval, 
                         "is a copy (half reads, half writes), which a read-heavy kernel can "
                         "exceed slightly"}
             for k in LINEAR_BYTES}
-        out["pair_fractions"] = {"f_in": fin, "f_lt_1.5": f15, "f_lt_0.5": f05}
+        out["pair_fractions"] = {"f_in": fin, "f_lt_1.5": f15, "f_lt_0.5": f05,
+                                 "source": "exact device count of the final state "
+                                           "(sph_pair_fractions, reference arithmetic)"}
         if world == 1 and args.cpu_baseline:
             out["cpu_baseline"] = cpu_baseline(ctx, store, grid, par, args)
     ctx.close()

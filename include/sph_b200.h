@@ -178,6 +178,12 @@ int sph_synchronize(sph_ctx *ctx);
 /* Measured FP64 FMA throughput of this device (TFLOP/s, 2 flops per DFMA). */
 int sph_fp64_peak(sph_ctx *ctx, double *tflops);
 
+/* Exact support fractions of the current state, a validation pass outside any timed
+ * region: out[0..2] = the shares of all active pairs (sum over cells of
+ * nl * na, out[3]) with q < 2.5, q < 1.5, q < 0.5, q = |x_i - x_j| / h_i by the reference's
+ * arithmetic (kernels.cpp:97-108). They fix the algorithmic flops per pair of bench.py. */
+int sph_pair_fractions(sph_ctx *ctx, double out[4]);
+
 /* ---- Device-resident slab decomposition (paper_2502_16517_b200/decomp.py) ----
  * The reference has no decomposition; these entry points let one context per GPU hold its
  * slab's particles on the device while the halo / migration traffic moves between GPUs as

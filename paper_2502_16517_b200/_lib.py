@@ -66,6 +66,7 @@ SIGNATURES = {
     "sph_get_stats": (C.c_int, [_vp, C.POINTER(SphStatsC)]),
     "sph_synchronize": (C.c_int, [_vp]),
     "sph_fp64_peak": (C.c_int, [_vp, C.POINTER(C.c_double)]),
+    "sph_pair_fractions": (C.c_int, [_vp, C.POINTER(C.c_double)]),
     "sph_launch_count": (C.c_int64, [_vp]),
     "sph_count": (C.c_int64, [_vp]),
     "sph_dd_count": (C.c_int, [_vp, _vp, C.POINTER(C.c_int64)]),

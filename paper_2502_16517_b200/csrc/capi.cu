@@ -2046,6 +2046,29 @@ int sph_synchronize(sph_ctx *ctx) {
   });
 }
 
+int sph_pair_fractions(sph_ctx *ctx, double out[4]) {
+  return guarded(ctx, [&] {
+    if (!ctx->bound) throw ArgError{"sph_pair_fractions before sph_bind"};
+    if (!out) throw ArgError{"null argument"};
+    if (ctx->need_rebin) throw ArgError{"particles were appended: call sph_rebin first"};
+    ctx->make_soa_current();
+    ctx->sync_items0();
+    DevBuf<unsigned long long> cnt;
+    cnt.ensure(3);
+    launch_pair_fractions(ctx->geom(), ctx->items0.p, ctx->n_items0, ctx->ilist.p, ctx->soa, cnt.p,
+                          ctx->stream);
+    ctx->launched();
+    unsigned long long h[3] = {0, 0, 0};
+    CK(cudaMemcpyAsync(h, cnt.p, sizeof h, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    cnt.release();
+    const double tot = (double)ctx->active_pairs;
+    for (int k = 0; k < 3; ++k) out[k] = tot > 0 ? (double)h[k] / tot : 0.0;
+    out[3] = tot;
+    return SPH_OK;
+  });
+}
+
 int sph_fp64_peak(sph_ctx *ctx, double *tflops) {
   return guarded(ctx, [&] {
     int sms = 0;

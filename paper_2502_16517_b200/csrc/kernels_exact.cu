@@ -395,4 +395,55 @@ void launch_eos(Particle *p, int n, double gamma, cudaStream_t s) {
   eos_kernel<<<(n + 255) / 256, 256, 0, s>>>(p, n, gamma);
 }
 
+// Exact support fractions of the current state ("count f_* exactly per run,
+// device counters in a validation pass"): over every active pair (i, j) of every local i,
+// q = sqrt(r2) * (1/h_i) by the reference's arithmetic (kernels.cpp:24, :100-105: minimum
+// image, r2 without contraction, IEEE sqrt and division; this file is built with
+// --fmad=false) and counts of q < 2.5, < 1.5, < 0.5 (r2 > 0). One warp per work item, lane =
+// local, every lane reading the same j (broadcast). Not on the timed path.
+__global__ void __launch_bounds__(128) pair_fraction_kernel(Geom g, const Item *items, int n_items,
+                                                            const int *list, SoaMirror f,
+                                                            unsigned long long *cnt) {
+  const int w = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  if (w >= n_items) return;
+  const Item it = items[w];
+  const bool live = lane < it.count;
+  const int slot = list[it.start + (live ? lane : 0)];
+  const double2 xi = f.x[slot];
+  const double inv_h = 1.0 / f.h[slot];
+  const Stencil st = make_stencil(it.cell, g.nx, g.ny);
+  unsigned c25 = 0, c15 = 0, c05 = 0;
+  for (int k = 0; k < st.n; ++k) {
+    const int b = g.cell_begin[st.cell[k]], e = g.cell_begin[st.cell[k] + 1];
+    for (int sj = b; sj < e; ++sj) {
+      const double2 xj = f.x[sj];
+      const double d0 = min_image(xi.x - xj.x), d1 = min_image(xi.y - xj.y);
+      const double r2 = d0 * d0 + d1 * d1;
+      if (!(r2 > 0.0)) continue;
+      const double q = sqrt(r2) * inv_h;
+      c25 += q < 2.5;
+      c15 += q < 1.5;
+      c05 += q < 0.5;
+    }
+  }
+  if (!live) c25 = c15 = c05 = 0;
+  for (int o = 16; o > 0; o >>= 1) {
+    c25 += __shfl_xor_sync(0xffffffffu, c25, o);
+    c15 += __shfl_xor_sync(0xffffffffu, c15, o);
+    c05 += __shfl_xor_sync(0xffffffffu, c05, o);
+  }
+  if (lane == 0) {
+    atomicAdd(cnt + 0, (unsigned long long)c25);
+    atomicAdd(cnt + 1, (unsigned long long)c15);
+    atomicAdd(cnt + 2, (unsigned long long)c05);
+  }
+}
+
+void launch_pair_fractions(const Geom &g, const Item *items, int n_items, const int *list,
+                           const SoaMirror &f, unsigned long long *cnt, cudaStream_t s) {
+  cudaMemsetAsync(cnt, 0, 3 * sizeof(unsigned long long), s);
+  if (n_items <= 0) return;
+  pair_fraction_kernel<<<(n_items + 3) / 4, 128, 0, s>>>(g, items, n_items, list, f, cnt);
+}
+
 } // namespace sphb

@@ -35,6 +35,9 @@ void launch_jview_force(double2 *xy, double2 *vv, double2 *mg, double2 *pv, doub
 void launch_linear(int kernel, bool aos, Particle *p, const SoaMirror &f, int n, const Params &par,
                    cudaStream_t s);
 void launch_eos(Particle *p, int n, double gamma, cudaStream_t s);
+// exact counts of active pairs with q < 2.5, < 1.5, < 0.5 (reference arithmetic) into cnt[3]
+void launch_pair_fractions(const Geom &g, const Item *items, int n_items, const int *list,
+                           const SoaMirror &f, unsigned long long *cnt, cudaStream_t s);
 
 // layout / bookkeeping kernels (kernels_layout.cu)
 // AoS -> SoA for the fields in `mask` (the paper's gather view) and SoA -> AoS scatter.

@@ -355,6 +355,13 @@ class Context:
         out["density_round_ms"] = list(s.density_round_ms)
         return out
 
+    def pair_fractions(self) -> tuple[float, float, float, float]:
+        """Exact shares of the active pairs with q < 2.5, < 1.5, < 0.5 in the current state
+        (reference arithmetic), and the active-pair count (sph_pair_fractions)."""
+        out = (C.c_double * 4)()
+        _check(self.h, self.lib.sph_pair_fractions(self.h, out), "sph_pair_fractions")
+        return out[0], out[1], out[2], out[3]
+
     def fp64_peak_tflops(self) -> float:
         v = C.c_double()
         _check(self.h, self.lib.sph_fp64_peak(self.h, C.byref(v)), "sph_fp64_peak")

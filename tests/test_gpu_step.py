@@ -399,3 +399,37 @@ def test_record_tails_follow_the_slots_across_layout_switches(orc):
         got = ctx.read_records()
     assert np.count_nonzero(ref["cell"] != recs0["cell"]) > 0, "particles must change cells"
     assert got.tobytes() == ref.tobytes()
+
+
+@pytest.mark.parametrize("kind", [0, 1])
+def test_pair_fractions_exact(orc, kind):
+    """sph_pair_fractions (the validation pass that fixes bench.py's algorithmic flops per
+    pair) counts the active pairs with q < 2.5, < 1.5, < 0.5 exactly as the reference computes
+    q (kernels.cpp:24, :100-105): equal to a float64 brute force over build_grid's lists."""
+    n, ppc, seed = 5000, 64, 4
+    recs, par = orc.make_particles(n, ppc, seed, kind=kind)
+    store = pkg.ParticleStore(recs, np.arange(n, dtype=np.int64), pkg.Layout.Continuous)
+    grid = pkg.build_grid(store, pkg.InitConfig(n=n, ppc=ppc))
+    with pkg.Context(0, numerics=Numerics.Fast, layout=DeviceLayout.Resident) as ctx:
+        ctx.bind(grid)
+        f_in, f15, f05, tot = ctx.pair_fractions()
+    nx = grid.nx
+    cb, li = grid.cell_begin, grid.local_idx
+    x = recs["x"]
+    inv_h = 1.0 / recs["h"]
+    counts = np.zeros(3, np.int64)
+    pairs = 0
+    for c in range(nx * nx):
+        loc = li[cb[c]:cb[c + 1]]
+        if not len(loc):
+            continue
+        act = cell_members(cb, li, stencil(c, nx, nx))
+        pairs += len(loc) * len(act)
+        d = x[loc][:, None, :] - x[act][None, :, :]
+        d = d - np.round(d)  # min_image (np.round is half-to-even; |d| < 1 here, no .5 ties)
+        r2 = d[..., 0] * d[..., 0] + d[..., 1] * d[..., 1]
+        q = np.sqrt(r2) * inv_h[loc][:, None]
+        ok = r2 > 0.0
+        counts += [np.count_nonzero(ok & (q < t)) for t in (2.5, 1.5, 0.5)]
+    assert tot == pairs
+    assert (f_in, f15, f05) == tuple(counts / pairs)
