@@ -67,8 +67,17 @@ def load_peaks():
     return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0}, "fallback"
 
 
-def load_pipe(kernel):
-    """FP64-pipe activity (%) of a kernel from the committed ncu capture."""
+def captured_workload(args):
+    """The committed ncu capture (tools/profile.sh) is of the default workload: BASELINE
+    config 2, 2^21 particles, ppc 1024, uniform IC, FAST numerics, resident layout."""
+    return (args.n, args.ppc, args.ic, args.numerics, args.layout) == (
+        1 << 21, 1024, "uniform", "fast", "resident")
+
+
+def load_pipe(kernel, args):
+    """FP64-pipe activity (%) of a kernel from the committed ncu capture (its workload only)."""
+    if not captured_workload(args):
+        return None
     p = os.path.join(ROOT, "profiles", "ncu_summary.json")
     try:
         with open(p) as f:
@@ -78,8 +87,11 @@ def load_pipe(kernel):
         return None
 
 
-def load_traffic():
-    """dram bytes per launch of the force kernel from the committed ncu capture."""
+def load_traffic(args):
+    """dram bytes per launch of the force kernel from the committed ncu capture; null for any
+    workload other than the captured one."""
+    if not captured_workload(args):
+        return None, "not captured for this workload (the ncu capture is of config 2)"
     p = os.path.join(ROOT, "profiles", "ncu_summary.json")
     try:
         with open(p) as f:
@@ -445,7 +457,7 @@ def _finish(out, ctx, store, grid, par, args, rank, world, ph, names, den_eval, 
         fpairs = workload_pairs / 2
         ach_f = ffl * fpairs / (ph[4] * 1e-3) / 1e12
         ach_d = dfl * (den_eval / args.steps) / (ph[3] * 1e-3) / 1e12
-        traffic, tsrc = load_traffic()
+        traffic, tsrc = load_traffic(args)
         out["roofline"] = {
             "bound": "fp64", "kernel": "force2_kernel", "achieved": ach_f,
             "peak": fp64, "unit": "TFLOP/s", "frac": ach_f / fp64, "traffic": traffic,
@@ -456,7 +468,7 @@ def _finish(out, ctx, store, grid, par, args, rank, world, ph, names, den_eval, 
             "note": "force evaluates gravity on every active pair (nothing culled), so this "
                     "is bounded by the FP64 pipe",
         }
-        pipe_f = load_pipe("force2_kernel")
+        pipe_f = load_pipe("force2_kernel", args)
         if pipe_f is not None:  # the hardware view beside the algorithmic-flop one
             out["roofline"]["fp64_pipe_pct_ncu"] = pipe_f
         cull_note = ("effective: the reference's algorithmic flops for every active pair "
@@ -473,7 +485,7 @@ def _finish(out, ctx, store, grid, par, args, rank, world, ph, names, den_eval, 
             "achieved": ach_i, "frac": ach_i / fp64, "flops_per_step": ins,
             "note": "flops of the in-support pairs only (every one is evaluated); a lower bound "
                     "of the work done, beside the 'effective' figure above, an upper one"}
-        pipe = load_pipe("density2_kernel")
+        pipe = load_pipe("density2_kernel", args)
         if pipe is not None:
             out["roofline_density"]["fp64_pipe_pct_ncu"] = pipe
         # the north-star figure: the whole step (density rounds + force + linear kernels +
